@@ -1,0 +1,206 @@
+"""CPU scorers for the oracle (TEST INFRASTRUCTURE).
+
+* ``SeededHashScorerCPU`` restates the reference's synthetic scorer
+  (bb/model.py:177-218: blake2b-keyed PCG64 logits, EOS logit
+  ``eos_bias*len/input_len``, fp64 log-softmax).  It is only used to pin this
+  oracle against outputs of the real reference (tests/golden).
+* ``HashLogitsCPU`` is the bit-exact CPU mirror of the product's device
+  synthetic scorer (paper_2010_02164_b200/csrc/hash_scorer.cu): a counter
+  hash of (seed, source, candidate prefix, token) -> fp32 (optionally bf16)
+  logits computed with IEEE-exact ops only, so CPU and GPU logits agree bit for
+  bit.
+* ``LseReplayScorer`` turns those logits into the rows the reference search
+  would see given the kernel's per-row ``lse``: ``float64(fp32(logit - lse))``
+  (SURVEY.md §7 hard part 2: the log-softmax contract).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+
+
+@dataclass(frozen=True, slots=True)
+class Encoding:
+    """bb/model.py:34-45."""
+
+    input_id: int
+    tokens: tuple
+    input_len: int
+    seed: int = 0
+
+
+def _check_input_tokens(tokens, vocab_size: int) -> tuple:
+    """bb/model.py:90-102."""
+    if len(tokens) == 0:
+        raise ValueError("inputs must be nonempty")
+    out = []
+    for pos, t in enumerate(tokens):
+        t = int(t)
+        if not (0 <= t < vocab_size):
+            raise ValueError(f"token {t} at position {pos} is outside the vocabulary "
+                             f"(size {vocab_size})")
+        out.append(t)
+    return tuple(out)
+
+
+class SeededHashScorerCPU:
+    """Restatement of bb/model.py:177-218 (SeededHashScorer)."""
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, seed: int, eos_bias: float = 0.0):
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self.seed = int(seed)
+        self.eos_bias = float(eos_bias)
+        self._key = struct.pack("<q", self.seed)
+
+    def _digest(self, tag: bytes, tokens: tuple, extra: int = 0) -> int:  # :195-198
+        payload = tag + struct.pack("<Q", extra) + struct.pack(f"<{len(tokens)}Q", *tokens)
+        return int.from_bytes(hashlib.blake2b(payload, digest_size=8, key=self._key).digest(),
+                              "little")
+
+    def encode(self, tokens, input_id: int = 0) -> Encoding:  # :200-207
+        checked = _check_input_tokens(tokens, self.vocab_size)
+        return Encoding(input_id, checked, len(checked), self._digest(b"enc", checked))
+
+    def score_next(self, enc: Encoding, cand):  # :209-218
+        if cand.finalized:
+            raise RuntimeError("scoring a finalized candidate")
+        state = self._digest(b"dec", tuple(cand.tokens), extra=enc.seed)
+        rng = np.random.Generator(np.random.PCG64(state))
+        logits = rng.random(self.vocab_size)
+        logits[self.eos] = self.eos_bias * len(cand.tokens) / enc.input_len
+        peak = logits.max()
+        return logits - (peak + math.log(np.exp(logits - peak).sum()))
+
+
+# ------------------------------------------------------ device scorer mirror
+def mix64(z: int) -> int:
+    """splitmix64 finalizer (same constants as csrc/hash_scorer.cu)."""
+    z &= M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def source_seed(seed: int, tokens) -> int:
+    h = mix64((seed ^ 0x9E3779B97F4A7C15) & M64)
+    for t in tokens:
+        h = mix64(h ^ ((int(t) + 0x632BE59BD9B4E019) & M64))
+    return h
+
+
+def prefix_init(src_seed: int, sos: int) -> int:
+    return mix64((src_seed + (sos + 1) * 0xD6E8FEB86659FD93) & M64)
+
+
+def prefix_step(h: int, token: int) -> int:
+    return mix64(h ^ (((token + 1) * 0xD6E8FEB86659FD93) & M64))
+
+
+def prefix_hash(src_seed: int, tokens) -> int:
+    h = prefix_init(src_seed, int(tokens[0]))
+    for t in tokens[1:]:
+        h = prefix_step(h, int(t))
+    return h
+
+
+def fmix32_np(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint32)
+    x ^= x >> np.uint32(16)
+    x *= np.uint32(0x85EBCA6B)
+    x ^= x >> np.uint32(13)
+    x *= np.uint32(0xC2B2AE35)
+    x ^= x >> np.uint32(16)
+    return x
+
+
+def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
+    """IEEE round-to-nearest-even fp32 -> bf16, returned widened to fp32
+    (matches __float2bfloat16_rn for finite values)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32)
+
+
+class HashLogitsCPU:
+    """Bit-exact CPU mirror of the device synthetic scorer's logits.
+
+    logit[v] = scale * u^power, u = (fmix32(key ^ v*0x9E3779B9) >> 8) * 2^-24
+    (key folds the candidate's prefix hash), and
+    logit[eos] = (eos_bias * len) / src_len, all fp32 round-to-nearest; in
+    bf16 mode each logit is then rounded to bf16.  Mirrors the structure of
+    bb/model.py:209-218 with an integer hash in place of blake2b+PCG64."""
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, seed: int, *, scale: float = 8.0,
+                 power: int = 1, eos_bias: float = 8.0, dtype: str = "f32"):
+        assert power in (1, 2, 4)
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self.seed, self.scale, self.power = int(seed), np.float32(scale), power
+        self.eos_bias, self.dtype = np.float32(eos_bias), dtype
+        self._v = np.arange(vocab_size, dtype=np.uint32) * np.uint32(0x9E3779B9)
+
+    def encode(self, tokens, input_id: int = 0) -> Encoding:
+        checked = tuple(int(t) for t in tokens)
+        if not checked:
+            raise ValueError("inputs must be nonempty")
+        return Encoding(input_id, checked, len(checked), source_seed(self.seed, checked))
+
+    def logits(self, enc: Encoding, tokens) -> np.ndarray:
+        h = prefix_hash(enc.seed, tokens)
+        key = np.uint32((h ^ (h >> 32)) & 0xFFFFFFFF)
+        bits = fmix32_np(self._v ^ key)
+        u = (bits >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+        if self.power >= 2:
+            u = u * u
+        if self.power >= 4:
+            u = u * u
+        x = (u * self.scale).astype(np.float32)
+        x[self.eos] = (self.eos_bias * np.float32(len(tokens))) / np.float32(enc.input_len)
+        if self.dtype == "bf16":
+            x = f32_to_bf16_rne(x)
+        return x
+
+    def score_next(self, enc: Encoding, cand):
+        """Standalone CPU rows (fp64 log-softmax of the fp32 logits, as the
+        reference does).  GPU parity uses LseReplayScorer instead."""
+        x = self.logits(enc, cand.tokens).astype(np.float64)
+        peak = x.max()
+        return x - (peak + math.log(np.exp(x - peak).sum()))
+
+
+class LseReplayScorer:
+    """Reference-protocol scorer whose rows are float64(fp32(logit - lse)),
+    with lse exported by the kernel per (input_id, tokens)."""
+
+    def __init__(self, base: HashLogitsCPU, lse_table: dict):
+        self.base = base
+        self.vocab_size, self.sos, self.eos = base.vocab_size, base.sos, base.eos
+        self.lse = lse_table
+
+    def encode(self, tokens, input_id: int = 0):
+        return self.base.encode(tokens, input_id)
+
+    def score_next(self, enc: Encoding, cand):
+        x = self.base.logits(enc, cand.tokens)
+        lse = np.float32(self.lse[(enc.input_id, tuple(cand.tokens))])
+        return (x - lse).astype(np.float32).astype(np.float64)
+
+
+class RowsScorer:
+    """tests/support.py:238-250: replays pre-drawn rows in call order."""
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, rows):
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self._rows = list(rows)
+
+    def encode(self, tokens, input_id: int = 0):
+        return Encoding(input_id, tuple(tokens), len(tokens))
+
+    def score_next(self, enc, cand):
+        return self._rows.pop(0)
