@@ -1,0 +1,112 @@
+// Shared device helpers for the VarStream sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/varstream.h"
+
+#define VS_LOG2E 1.4426950408889634f
+#define VS_LN2 0.6931471805599453f
+
+namespace vs {
+
+// ---- orderable encodings -------------------------------------------------
+// fp32 -> uint32 preserving total order (larger float -> larger uint).
+__device__ __forceinline__ uint32_t ord_f32(float x) {
+  if (x == 0.0f) x = 0.0f;  // canonicalise -0
+  uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ __forceinline__ uint64_t ord_f64(double x) {
+  if (x == 0.0) x = 0.0;
+  uint64_t u = (uint64_t)__double_as_longlong(x);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// 64-bit selection key of a row entry: (logp desc, token asc) == larger key first.
+__device__ __forceinline__ uint64_t row_key(float logp, int tok) {
+  return ((uint64_t)ord_f32(logp) << 32) | (uint64_t)(0xffffffffu - (uint32_t)tok);
+}
+__device__ __forceinline__ int key_tok(uint64_t k) { return (int)(0xffffffffu - (uint32_t)k); }
+__device__ __forceinline__ float key_logp(uint64_t k) { return unord_f32((uint32_t)(k >> 32)); }
+
+// ---- hashing (bit-identical to oracle/scorers.py) --------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t prefix_init(uint64_t src_seed, int sos) {
+  return mix64(src_seed + (uint64_t)(sos + 1) * 0xD6E8FEB86659FD93ull);
+}
+__host__ __device__ __forceinline__ uint64_t prefix_step(uint64_t h, int tok) {
+  return mix64(h ^ ((uint64_t)(tok + 1) * 0xD6E8FEB86659FD93ull));
+}
+__device__ __forceinline__ uint32_t fmix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return x;
+}
+
+// ---- loads -----------------------------------------------------------------
+// Streaming 16-byte load: read-only, do not allocate in L1 (each byte is read once).
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T x);
+template <>
+__device__ __forceinline__ float to_f32<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+
+// ---- warp helpers ------------------------------------------------------------
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+  uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    uint64_t o = shfl_xor_u64(v, m);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+// Online log-sum-exp pair merge: (m, s) with s = sum exp(x - m).
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;  // both empty
+  float a = (m == -INFINITY) ? 0.0f : s * exp2f((m - mn) * VS_LOG2E);
+  float b = (m2 == -INFINITY) ? 0.0f : s2 * exp2f((m2 - mn) * VS_LOG2E);
+  m = mn;
+  s = a + b;
+}
+
+}  // namespace vs
+
+#define VS_CUDA_RET()                                              \
+  do {                                                             \
+    cudaError_t _e = cudaGetLastError();                           \
+    return _e == cudaSuccess ? VS_OK : VS_ERR_CUDA;                \
+  } while (0)

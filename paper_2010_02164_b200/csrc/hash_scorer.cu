@@ -1,0 +1,103 @@
+// Synthetic device scorer: deterministic logits for every scored row.
+//
+// Stands in for the decoder's vocab projection in the search benchmark. It
+// mirrors the structure of the reference's SeededHashScorer
+// (bb/model.py:177-218): logits are a pure function of (seed, source,
+// candidate prefix, token) and the EOS logit is eos_bias * len / src_len,
+// but the generator is a counter hash (splitmix64 / murmur3 fmix32) built
+// from IEEE-exact operations only, so oracle/scorers.py:HashLogitsCPU
+// reproduces every logit bit for bit on the CPU.
+#include "common.cuh"
+
+namespace vs {
+namespace {
+
+__global__ void hash_encode_kernel(vs_config cfg, vs_state st, uint64_t seed) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nadm = st.status[VS_ST_NADMIT];
+  if (i >= nadm) return;
+  const int s = st.status[VS_ST_HDR + 3 * cfg.n + i];
+  const int input = st.slot_input[s];
+  uint64_t h = mix64(seed ^ 0x9E3779B97F4A7C15ull);
+  for (int p = st.src_off[input]; p < st.src_off[input + 1]; ++p)
+    h = mix64(h ^ ((uint64_t)st.src_tok[p] + 0x632BE59BD9B4E019ull));
+  st.slot_seed[s] = h;
+  st.c_hash[s * cfg.k] = prefix_init(h, cfg.sos);
+}
+
+__device__ __forceinline__ float hash_logit(uint32_t key, int v, float scale, int power) {
+  const uint32_t bits = fmix32(((uint32_t)v * 0x9E3779B9u) ^ key);
+  float u = __fmul_rn((float)(bits >> 8), 5.9604644775390625e-08f);  // * 2^-24, exact
+  if (power >= 2) u = __fmul_rn(u, u);
+  if (power >= 4) u = __fmul_rn(u, u);
+  return __fmul_rn(u, scale);
+}
+
+template <typename T>
+__device__ __forceinline__ T cvt(float x);
+template <>
+__device__ __forceinline__ float cvt<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+// grid: (chunks of 8*NT columns, rows); 8 consecutive tokens per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_state st, vs_hash_params hp,
+                                                          T* __restrict__ logits, int64_t ld) {
+  const int r = blockIdx.y;
+  if (r >= st.status[VS_ST_R]) return;
+  const int V = cfg.vocab_size;
+  const int v0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (v0 >= V) return;
+  const int s = st.row_slot[r];
+  const uint64_t h = st.c_hash[s * cfg.k + st.row_cand[r]];
+  const uint32_t key = (uint32_t)(h ^ (h >> 32));
+  const float eos_val = __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
+  T* out = logits + (int64_t)r * ld;
+  T vals[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int v = v0 + j;
+    const float x = (v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power);
+    vals[j] = cvt<T>(x);
+  }
+  const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
+  if (vec_ok) {
+    if (sizeof(T) == 2) {
+      *reinterpret_cast<uint4*>(out + v0) = *reinterpret_cast<const uint4*>(vals);
+    } else {
+      reinterpret_cast<uint4*>(out + v0)[0] = reinterpret_cast<const uint4*>(vals)[0];
+      reinterpret_cast<uint4*>(out + v0)[1] = reinterpret_cast<const uint4*>(vals)[1];
+    }
+  } else {
+    for (int j = 0; j < 8 && v0 + j < V; ++j) out[v0 + j] = vals[j];
+  }
+}
+
+}  // namespace
+}  // namespace vs
+
+extern "C" int vs_hash_encode(const vs_config* cfg, const vs_state* st, uint64_t seed, void* stream) {
+  if (!cfg || !st) return VS_ERR_CONFIG;
+  const int n = cfg->n;
+  vs::hash_encode_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(*cfg, *st, seed);
+  VS_CUDA_RET();
+}
+
+extern "C" int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs_hash_params* hp,
+                              void* logits, int64_t ld, int32_t R_grid, void* stream) {
+  if (!cfg || !st || !hp || !logits || ld < cfg->vocab_size) return VS_ERR_CONFIG;
+  if (hp->power != 1 && hp->power != 2 && hp->power != 4) return VS_ERR_CONFIG;
+  if (R_grid <= 0) return VS_OK;
+  if (R_grid > 65535) return VS_ERR_CONFIG;
+  const int cols = (cfg->vocab_size + 8 * 256 - 1) / (8 * 256);
+  dim3 grid(cols, R_grid);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (hp->dtype == VS_DTYPE_F32)
+    vs::hash_logits_kernel<float><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<float*>(logits), ld);
+  else if (hp->dtype == VS_DTYPE_BF16)
+    vs::hash_logits_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<__nv_bfloat16*>(logits), ld);
+  else
+    return VS_ERR_CONFIG;
+  VS_CUDA_RET();
+}

@@ -1,0 +1,320 @@
+"""Device-resident VarStream engine: one refilling batch per GPU.
+
+Replaces the body of the reference driver (bb/scheduler.py:243-287 `_drive`
+and `_execute_step` :168-205).  All beam state lives in HBM in the SoA layout
+of include/varstream.h; the host only launches kernels and reads a small
+status record per step:
+
+    vs_schedule   (K3)  stable removal of finished beams, ε-refill, selection,
+                        next step's row list                 -> status
+    scorer.logits       decoder / synthetic scorer for the R_t rows
+    vs_row_lse_topm (K1) fused log-softmax + per-row top-M
+    vs_beam_step  (K2)  per-beam merge / δ,M prune / finalise / emit / drain
+    scorer.after_step   K4 row-state reorder from K2's copy plan
+
+Two drivers: ``run`` (one status read per step; supports flush, StepEvent
+callbacks and traces — the drop-in path) and ``run_async`` (no per-step host
+sync: kernels take R_t from device memory and the host trails the device by
+a ring of status snapshots; used for throughput).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import Candidate, DecodeConfig, FinalizationPolicy, Vocabulary
+from .errors import ConfigError, InvariantViolation
+from .metrics import CostParams, MetricsReport
+
+
+@dataclass(frozen=True)
+class StepEvent:
+    """Observability record per step (bb/scheduler.py:77-88)."""
+
+    timestep: int
+    phase: str
+    refilled: tuple
+    selected: tuple
+    expansions: int
+    effective_len: int
+    finished: tuple
+    live_after: tuple
+
+
+def refill_threshold(config: DecodeConfig) -> int:
+    """bb/scheduler.py:237-240: integer form of live <= eps*n."""
+    return math.floor(config.epsilon * config.n + 1e-9)
+
+
+class DecodeResults(Sequence):
+    """Per-input emitted candidates, in input order (bb/scheduler.py:287),
+    built lazily from the device output buffers copied back to the host."""
+
+    def __init__(self, count, lens, scores, toks, k: int, max_len: int):
+        self.count, self.lens, self.scores, self.toks = count, lens, scores, toks
+        self.k, self.max_len = k, max_len
+
+    def __len__(self) -> int:
+        return int(self.count.shape[0])
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        out = []
+        for e in range(int(self.count[i])):
+            o = i * self.k + e
+            n = int(self.lens[o])
+            out.append(Candidate(tuple(int(t) for t in self.toks[o, :n]), float(self.scores[o]),
+                                 True, i))
+        return out
+
+
+class SearchEngine:
+    """Owns the device state of one refilling batch (n beam slots x k rows)."""
+
+    def __init__(self, config: DecodeConfig, vocab: Vocabulary, *, device=None,
+                 m_rows: int | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2010_02164_b200 requires a CUDA device (sm_100a); "
+                               "there is no CPU fallback")
+        if config.policy is not FinalizationPolicy.DEFERRED:
+            raise ConfigError("the device engine implements the deferred policy "
+                              "(immediate is listed as next work in DESIGN.md)")
+        if config.k > N.VS_MAX_K or config.n > N.VS_MAX_SLOTS or config.max_candidates > N.VS_MAX_M:
+            raise ConfigError(f"k<= {N.VS_MAX_K}, n <= {N.VS_MAX_SLOTS}, M <= {N.VS_MAX_M} "
+                              "in this build")
+        self.lib = N.load_library()
+        self.config, self.vocab = config, vocab
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        k, n, L = config.k, config.n, config.max_len
+        self.k, self.n, self.max_len = k, n, L
+        self.capacity = min(config.capacity, n * k)  # a step can never need more rows
+        self.m_rows = m_rows or min(config.max_candidates, vocab.size)
+        dev = self.device
+        i32 = dict(dtype=torch.int32, device=dev)
+        z = torch.zeros
+        self.t = {
+            "slot_input": z(n, **i32), "slot_lt": z(n, **i32), "slot_emitted": z(n, **i32),
+            "slot_width": z(n, **i32), "slot_active": z(n, **i32), "slot_src_len": z(n, **i32),
+            "slot_flags": z(n, **i32), "slot_seed": z(n, dtype=torch.int64, device=dev),
+            "c_score": z(n * k, dtype=torch.float64, device=dev), "c_len": z(n * k, **i32),
+            "c_row": z(n * k, **i32), "c_fin": z(n * k, dtype=torch.uint8, device=dev),
+            "c_hash": z(n * k, dtype=torch.int64, device=dev), "hist": z(n * k * L, **i32),
+            "live": z(n, **i32), "counters": z(8, **i32), "sel": z(n, **i32),
+            "sel_off": z(n + 1, **i32), "row_slot": z(self.capacity, **i32),
+            "row_cand": z(self.capacity, **i32), "row_phys": z(self.capacity, **i32),
+            "row_len": z(self.capacity, **i32),
+            "top_tok": z(self.capacity * self.m_rows, **i32),
+            "top_logp": z(self.capacity * self.m_rows, dtype=torch.float32, device=dev),
+            "row_lse": z(self.capacity, dtype=torch.float32, device=dev),
+            "copy_list": z(self.capacity * 3, **i32), "n_copy": z(1, **i32),
+            "status": z(N.status_ints(n), **i32), "fallbacks": z(1, **i32),
+        }
+        self.status_host = torch.zeros(N.status_ints(n), dtype=torch.int32, pin_memory=True)
+        self.cfg = N.VsConfig(k=k, n=n, max_candidates=config.max_candidates, max_len=L,
+                              vocab_size=vocab.size, sos=vocab.sos, eos=vocab.eos,
+                              policy=N.VS_POLICY_DEFERRED, capacity=self.capacity,
+                              refill_threshold=refill_threshold(config), delta=config.delta)
+        self.state = N.VsState()
+        for f in N.STATE_FIELDS:
+            if f in self.t:
+                setattr(self.state, f, self.t[f].data_ptr())
+        self.N = 0
+
+    # ------------------------------------------------------------------ data
+    @property
+    def stream_ptr(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def load_corpus(self, corpus, *, src_tok=None, src_off=None) -> None:
+        """Copy the (length-bucketed) input stream to HBM and size the outputs.
+        Pass ``src_tok``/``src_off`` (pinned host or device int32) to skip the
+        Python flattening."""
+        if src_off is None:
+            lens = np.fromiter((len(x) for x in corpus), dtype=np.int64, count=len(corpus))
+            src_off = np.zeros(len(corpus) + 1, dtype=np.int32)
+            np.cumsum(lens, out=src_off[1:])
+            src_tok = np.fromiter((t for x in corpus for t in x), dtype=np.int32,
+                                  count=int(src_off[-1]))
+        if isinstance(src_off, np.ndarray):
+            src_off, src_tok = torch.from_numpy(src_off), torch.from_numpy(src_tok)
+        n_in = int(src_off.shape[0]) - 1
+        if n_in < 1:
+            raise ConfigError("corpus must be nonempty")
+        self.N = n_in
+        dev = self.device
+        self.t["src_off"] = src_off.to(dev, non_blocking=True)
+        self.t["src_tok"] = (src_tok if src_tok.numel() else torch.zeros(1, dtype=torch.int32)).to(
+            dev, non_blocking=True)
+        k, L = self.k, self.max_len
+        self.t["out_count"] = torch.zeros(n_in, dtype=torch.int32, device=dev)
+        self.t["out_len"] = torch.zeros(n_in * k, dtype=torch.int32, device=dev)
+        self.t["out_score"] = torch.zeros(n_in * k, dtype=torch.float64, device=dev)
+        self.t["out_tok"] = torch.zeros(n_in * k * L, dtype=torch.int32, device=dev)
+        for f in ("src_off", "src_tok", "out_count", "out_len", "out_score", "out_tok"):
+            setattr(self.state, f, self.t[f].data_ptr())
+
+    def results(self) -> DecodeResults:
+        """D2H of the output buffers (pinned) -> lazily materialised candidates."""
+        k, L, n_in = self.k, self.max_len, self.N
+        host = {f: torch.empty(self.t[f].shape, dtype=self.t[f].dtype, pin_memory=True)
+                for f in ("out_count", "out_len", "out_score", "out_tok")}
+        for f, h in host.items():
+            h.copy_(self.t[f], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return DecodeResults(host["out_count"].numpy(), host["out_len"].numpy(),
+                             host["out_score"].numpy(), host["out_tok"].numpy().reshape(n_in * k, L),
+                             k, L)
+
+    # --------------------------------------------------------------- kernels
+    def schedule(self, *, first: bool, remove: bool, admit: int, select: int) -> None:
+        N.check(self.lib.vs_schedule(C.byref(self.cfg), C.byref(self.state), self.N, int(first),
+                                     int(remove), admit, select, self.stream_ptr), "vs_schedule")
+
+    def read_status(self) -> np.ndarray:
+        self.status_host.copy_(self.t["status"], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        st = self.status_host.numpy()
+        if st[N.ST_ERROR] == N.VS_ERR_CONFIG:
+            raise ConfigError("a single beam needs more expansions than the step capacity")
+        if st[N.ST_ERROR]:
+            raise InvariantViolation(f"device scheduler error {int(st[N.ST_ERROR])}")
+        return st
+
+    def row_topm(self, logits: torch.Tensor, dtype_code: int, R_host: int, R_grid: int,
+                 d_R: int | None = None) -> None:
+        ld = logits.stride(0)
+        N.check(self.lib.vs_row_lse_topm(
+            logits.data_ptr(), dtype_code, ld, self.vocab.size, self.m_rows, R_host, d_R, R_grid,
+            self.t["top_tok"].data_ptr(), self.t["top_logp"].data_ptr(), self.t["row_lse"].data_ptr(),
+            self.t["fallbacks"].data_ptr(), self.stream_ptr), "vs_row_lse_topm")
+
+    def beam_step(self) -> None:
+        N.check(self.lib.vs_beam_step(C.byref(self.cfg), C.byref(self.state), self.m_rows,
+                                      self.stream_ptr), "vs_beam_step")
+
+    def status_ptr(self, idx: int) -> int:
+        return self.t["status"].data_ptr() + 4 * idx
+
+    # ---------------------------------------------------------------- drivers
+    def _step(self, scorer, st: np.ndarray, *, phase: str) -> None:
+        R = int(st[N.ST_R])
+        if phase == "stream" and st[N.ST_NADMIT] > 0:
+            scorer.on_admit(self, st)
+        logits, code = scorer.logits(self, R)
+        self.row_topm(logits, code, R, R)
+        self.beam_step()
+        scorer.after_step(self, R)
+
+    def run(self, corpus, scorer, *, admit_mode: int, select_mode: int, flush_enabled: bool,
+            trace: bool = False, on_step: Callable | None = None):
+        """Synchronous driver mirroring bb/scheduler.py:243-287 step for step."""
+        cfgd = self.config
+        self.load_corpus(corpus)
+        scorer.bind(self)
+        report = MetricsReport.new(trace=trace)
+        cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
+        n = self.n
+        timestep = 0
+        next_flush = cfgd.flush_interval if flush_enabled and cfgd.flush_interval else None
+        pending = None  # event fields of the last executed step, awaiting removal info
+        removed, first = True, True
+
+        def close_event(st):
+            nonlocal pending
+            if pending is not None and on_step is not None:
+                h = N.ST_HDR
+                fin = tuple(int(x) for x in st[h + n:h + n + st[N.ST_NFIN]])
+                live = tuple(int(x) for x in st[h + 2 * n:h + 2 * n + st[N.ST_NLIVE_AFTER]])
+                on_step(StepEvent(*pending, fin, live))
+            pending = None
+
+        def execute(st, phase, refilled):
+            nonlocal timestep, pending
+            self._step(scorer, st, phase=phase)
+            timestep += 1
+            R, L = int(st[N.ST_R]), int(st[N.ST_L])
+            report.record_step(R, L, cost)
+            sel = tuple(int(x) for x in st[N.ST_HDR:N.ST_HDR + st[N.ST_NSEL]])
+            pending = (timestep, phase, refilled, sel, R, L)
+
+        while True:
+            if next_flush is not None and timestep >= next_flush:  # bb/scheduler.py:262-265
+                self.schedule(first=first, remove=not removed, admit=N.VS_ADMIT_NONE,
+                              select=N.VS_SELECT_ALL)
+                first, removed = False, True
+                st = self.read_status()
+                close_event(st)
+                while st[N.ST_NLIVE] > 0:
+                    execute(st, "flush", ())
+                    self.schedule(first=False, remove=True, admit=N.VS_ADMIT_NONE,
+                                  select=N.VS_SELECT_ALL)
+                    st = self.read_status()
+                    close_event(st)
+                next_flush = timestep + cfgd.flush_interval
+            self.schedule(first=first, remove=not removed, admit=admit_mode, select=select_mode)
+            first, removed = False, True
+            st = self.read_status()
+            close_event(st)
+            if st[N.ST_NLIVE] == 0:
+                break
+            a0, na = int(st[N.ST_ADMIT0]), int(st[N.ST_NADMIT])
+            execute(st, "stream", tuple(range(a0, a0 + na)))
+            removed = False
+        if st[N.ST_CURSOR] != self.N:
+            raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
+        return self.results(), report
+
+    def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
+                  ring: int = 8, trace: bool = False, src_tok=None, src_off=None,
+                  materialize: bool = True):
+        """Host-sync-free driver (no flush / no StepEvents): every kernel reads
+        R_t from device memory, status headers are streamed into a pinned ring
+        and consumed `ring` steps behind the device."""
+        cfgd = self.config
+        self.load_corpus(corpus, src_tok=src_tok, src_off=src_off)
+        scorer.bind(self)
+        report = MetricsReport.new(trace=trace)
+        cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
+        hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
+        events = [torch.cuda.Event() for _ in range(ring)]
+        stream = torch.cuda.current_stream(self.device)
+        cap = self.capacity
+        d_R = self.status_ptr(N.ST_R)
+        launched = processed = 0
+        done = False
+        self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode)
+        while not done:
+            slot = launched % ring
+            if launched - processed >= ring:  # consume the oldest snapshot
+                events[processed % ring].synchronize()
+                st = hdr[processed % ring].numpy()
+                if st[N.ST_ERROR]:
+                    self.read_status()
+                if st[N.ST_NLIVE] == 0:
+                    done = True
+                    break
+                report.record_step(int(st[N.ST_R]), int(st[N.ST_L]), cost)
+                processed += 1
+            hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
+            events[slot].record(stream)
+            scorer.on_admit(self, None)
+            logits, code = scorer.logits(self, None)
+            self.row_topm(logits, code, 0, cap, d_R)
+            self.beam_step()
+            scorer.after_step(self, None)
+            self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
+            launched += 1
+        st = self.read_status()
+        if st[N.ST_CURSOR] != self.N:
+            raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
+        return (self.results() if materialize else None), report

@@ -1,0 +1,77 @@
+"""Batched decoding drivers (drop-ins for bb/scheduler.py:290-367 and
+bb/harness.py:241-260), executed by the device engine.
+
+Signatures match the reference: ``run_varstream(corpus, scorer, config, *,
+trace=False, on_step=None) -> (outputs, MetricsReport)`` where outputs[i] is
+the list of Candidates emitted for input i (in input order).  ``scorer`` may
+be a BatchedScorer (device) or any reference-protocol Scorer
+(bb/model.py:78-87), which is wrapped in HostScorerAdapter.
+"""
+
+from __future__ import annotations
+
+import math
+
+from . import _native as N
+from .core import DecodeConfig, Vocabulary
+from .engine import SearchEngine
+from .errors import ConfigError
+from .scorers import HostScorerAdapter
+
+ENGINES = ("fixed", "varbeam", "varstream", "varfifo", "fixedstream")
+_PRUNING_OFF = {"fixed": "varbeam", "fixedstream": "varstream"}
+
+
+def _as_batched(scorer, corpus):
+    if all(hasattr(scorer, a) for a in ("bind", "on_admit", "logits", "after_step")):
+        return scorer
+    return HostScorerAdapter(scorer, corpus)
+
+
+def _vocab(scorer) -> Vocabulary:
+    v = scorer.vocab
+    return v if isinstance(v, Vocabulary) else Vocabulary(v.size, v.sos, v.eos)
+
+
+def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast):
+    if not len(corpus):
+        raise ConfigError("corpus must be nonempty")
+    bs = _as_batched(scorer, corpus)
+    eng = SearchEngine(config, _vocab(bs))
+    if fast and on_step is None and not (flush and config.flush_interval):
+        if not isinstance(bs, HostScorerAdapter):
+            return eng.run_async(corpus, bs, admit_mode=admit, select_mode=select, trace=trace)
+    return eng.run(corpus, bs, admit_mode=admit, select_mode=select, flush_enabled=flush,
+                   trace=trace, on_step=on_step)
+
+
+def run_varstream(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on_step=None,
+                  fast: bool = True):
+    """ε-refill + min-l_t selection (bb/scheduler.py:314-340)."""
+    return _run(corpus, scorer, config, N.VS_ADMIT_VARSTREAM, N.VS_SELECT_MIN_LT, True, trace,
+                on_step, fast)
+
+
+def run_varbeam(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on_step=None,
+                fast: bool = True):
+    """Traditional batching: admit only when empty (bb/scheduler.py:290-311)."""
+    return _run(corpus, scorer, config, N.VS_ADMIT_VARBEAM, N.VS_SELECT_MIN_LT, False, trace,
+                on_step, fast)
+
+
+def run_varfifo(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on_step=None,
+                fast: bool = True):
+    """Always-full batch, most-advanced first (bb/scheduler.py:343-367)."""
+    return _run(corpus, scorer, config, N.VS_ADMIT_VARFIFO, N.VS_SELECT_FIFO, False, trace,
+                on_step, fast)
+
+
+def dispatch_engine(engine: str, corpus, scorer, config: DecodeConfig, *, trace: bool = False):
+    """bb/harness.py:241-260 (greedy is out of scope for the device path)."""
+    runner = {"fixed": run_varbeam, "varbeam": run_varbeam, "varstream": run_varstream,
+              "fixedstream": run_varstream, "varfifo": run_varfifo}.get(engine)
+    if runner is None:
+        raise ConfigError(f"unknown engine {engine!r}")
+    if engine in _PRUNING_OFF and (config.delta != math.inf or config.max_candidates != config.k):
+        raise ConfigError(f"engine {engine!r} requires pruning off: delta=inf and max_candidates=k")
+    return runner(corpus, scorer, config, trace=trace)

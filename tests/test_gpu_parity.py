@@ -1,0 +1,257 @@
+"""GPU parity: the sm_100a kernels vs the CPU oracle (pinned to the reference).
+
+All calls go through the C-ABI library (paper_2010_02164_b200/_lib/libvarstream.so).
+Contract (BASELINE.json north_star): given identical logits, top-k indices,
+prune/finalise decisions and refill order are bit-exact; fp64 scores are
+bit-exact given the kernel's exported lse (logp = fp32(logit - lse)); lse
+itself agrees with an fp64 log-softmax within 1e-5 relative.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from goldens import fl, load
+from oracle import varstream_oracle as O
+from oracle.scorers import HashLogitsCPU, LseReplayScorer, SeededHashScorerCPU
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _pkg():
+    import paper_2010_02164_b200 as P
+    from paper_2010_02164_b200 import _native as N
+    from paper_2010_02164_b200.engine import SearchEngine
+    from paper_2010_02164_b200.scorers import DeviceHashScorer, HostScorerAdapter, LseRecorder
+
+    return P, N, SearchEngine, DeviceHashScorer, HostScorerAdapter, LseRecorder
+
+
+def _check_rows(x32: np.ndarray, M: int, tok, lp, lse, normalized=False):
+    R, V = x32.shape
+    x64 = x32.astype(np.float64)
+    for r in range(R):
+        l = np.float32(0.0) if normalized else np.float32(lse[r])
+        logp = (x32[r] - l).astype(np.float32)
+        want = O.row_top_m(logp.astype(np.float64), M)
+        m = min(M, V)
+        assert list(tok[r, :m]) == list(want), f"row {r}"
+        assert np.array_equal(lp[r, :m], logp[want]), f"row {r}"
+        if not normalized and np.isfinite(x64[r]).any():
+            peak = x64[r].max()
+            ref = peak + math.log(np.exp(x64[r] - peak).sum())
+            assert abs(float(lse[r]) - ref) <= 1e-5 * max(1.0, abs(ref)), f"row {r} lse"
+
+
+CASES = [(1000, 3), (1000, 5), (2048, 10), (42024, 5), (42024, 50), (17, 3), (3, 5), (4096, 1),
+         (33, 16), (1001, 64)]
+
+
+@pytest.mark.parametrize("V,M", CASES)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_row_topm_matches_oracle(V, M, dtype):
+    P, *_ = _pkg()
+    rng = np.random.default_rng(V * 131 + M)
+    R = 24
+    x = rng.normal(0, 3, (R, V)).astype(np.float32)
+    x[1] = np.round(x[1] * 2) / 2             # heavy ties
+    x[2] = 0.25                               # uniform row -> exact fallback
+    x[3, ::3] = -np.inf                       # masked tokens
+    x[4] = x[4] * 1e-3 + 40.0                 # near-equal logits that merge after - lse
+    x[5, :] = -np.inf
+    x[5, V // 2] = 1.0                        # one finite entry
+    x[6] = np.float32(1e6) + x[6]             # large offset
+    t = torch.from_numpy(x).cuda()
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16)
+        x = t.float().cpu().numpy()
+    tok, lp, lse, fb = P.row_lse_topm(t, M)
+    torch.cuda.synchronize()
+    _check_rows(x, M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
+
+
+def test_row_topm_strided_and_normalized_rows():
+    P, *_ = _pkg()
+    rng = np.random.default_rng(3)
+    big = torch.from_numpy(rng.uniform(-9, 0, (16, 1040)).astype(np.float32)).cuda()
+    view = big[:, :1000]  # ld = 1040
+    tok, lp, lse, _ = P.row_lse_topm(view, 7, normalized=True)
+    _check_rows(view.cpu().numpy(), 7, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy(),
+                normalized=True)
+    assert float(lse.abs().max()) == 0.0
+
+
+EXPAND = [c for c in load("expand_cases.json") if c["config"]["policy"] == "deferred"]
+
+
+def _ocfg(d):
+    return O.OConfig(k=d["k"], n=d["n"], epsilon=d["epsilon"], delta=fl(d["delta"]),
+                     max_candidates=d["max_candidates"], max_len=d["max_len"], policy=d["policy"])
+
+
+def test_device_expand_beam_matches_reference_goldens():
+    """Every deferred golden case of the reference's expand_beam (incl. the
+    row-value pre-truncation gap case) through K1+K2 on the device."""
+    P, *_ = _pkg()
+    for ci, case in enumerate(EXPAND):
+        d = case["config"]
+        cfg = P.DecodeConfig(k=d["k"], n=1, delta=fl(d["delta"]), max_candidates=d["max_candidates"],
+                             max_len=d["max_len"], policy="deferred")
+        v = case["vocab"]
+        vocab = P.Vocabulary(v["size"], v["sos"], v["eos"])
+        cands = tuple(P.Candidate(tuple(c["tokens"]), fl(c["score"]), c["finalized"])
+                      for c in case["beam"]["candidates"])
+        beam = P.Beam(0, cands, case["beam"]["l_t"], case["beam"]["emitted"])
+        rows = [[fl(x) for x in r] for r in case["rows"]]
+        got, emitted = P.expand_beam(beam, rows, cfg, vocab)
+        # oracle on the fp32-rounded rows the kernel contract sees
+        r32 = [np.asarray(r, dtype=np.float32).astype(np.float64) for r in rows]
+        ob = O.Beam(0, tuple(O.Candidate(c.tokens, c.score, c.finalized) for c in cands),
+                    beam.l_t, beam.emitted)
+        want, wem = O.expand_beam(ob, r32, _ocfg(d), v["size"], v["eos"])
+        key = lambda c: (tuple(c.tokens), c.score, bool(c.finalized))  # noqa: E731
+        assert [key(c) for c in got.candidates] == [key(c) for c in want.candidates], ci
+        assert [(c.tokens, c.score) for c in emitted] == [(c.tokens, c.score) for c in wem], ci
+        assert got.emitted == want.emitted
+        if all(float(np.float32(x)) == x for r in rows for x in r):  # fp32-exact rows
+            assert [key(c) for c in got.candidates] == [
+                (tuple(c["tokens"]), fl(c["score"]), c["finalized"]) for c in case["want"]["next"]]
+
+
+def _events(evs):
+    return [(e.timestep, e.phase, tuple(e.refilled), tuple(e.selected), e.expansions,
+             e.effective_len, tuple(e.finished), tuple(e.live_after)) for e in evs]
+
+
+class _F32Rows:
+    """Oracle-side view of a reference scorer with rows rounded to fp32 (the
+    device adapter uploads fp32 rows)."""
+
+    def __init__(self, inner):
+        self.inner = inner
+        self.vocab_size, self.sos, self.eos = inner.vocab_size, inner.sos, inner.eos
+
+    def encode(self, tokens, input_id=0):
+        return self.inner.encode(tokens, input_id)
+
+    def score_next(self, enc, cand):
+        return np.asarray(self.inner.score_next(enc, cand), dtype=np.float32).astype(np.float64)
+
+
+class _RefVocabScorer:
+    """SeededHashScorerCPU exposing a reference-style .vocab for the adapter."""
+
+    def __init__(self, inner, vocab):
+        self.inner, self.vocab = inner, vocab
+
+    def encode(self, tokens, input_id=0):
+        return self.inner.encode(tokens, input_id)
+
+    def score_next(self, enc, cand):
+        return self.inner.score_next(enc, cand)
+
+
+RUNS = {f["name"]: f for f in load("runs.json")}
+
+
+@pytest.mark.parametrize("name", ["c1_varstream_eps0.1667", "c1_varbeam", "c1_varfifo",
+                                  "c1_varstream_flush7", "c1_varstream_cap23", "c1_fixedstream"])
+def test_engine_with_reference_scorer_matches_oracle_events(name):
+    """Reference workloads (SeededHashScorer) through the device engine via the
+    drop-in adapter: StepEvents, trace and outputs bit-exact vs the oracle
+    given the same (fp32) rows."""
+    P, N, SearchEngine, _, HostScorerAdapter, _ = _pkg()
+    fx = RUNS[name]
+    s = fx["scorer"]
+    base = SeededHashScorerCPU(s["vocab_size"], s["sos"], s["eos"], s["seed"], s["eos_bias"])
+    d = fx["config"]
+    cfg = P.DecodeConfig(k=d["k"], n=d["n"], epsilon=d["epsilon"], delta=fl(d["delta"]),
+                         max_candidates=d["max_candidates"], max_len=d["max_len"],
+                         capacity=d["capacity"], flush_interval=d["flush_interval"])
+    corpus = [tuple(x) for x in fx["corpus"]][:120]
+    vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
+    runner = {"run_varstream": P.run_varstream, "run_varbeam": P.run_varbeam,
+              "run_varfifo": P.run_varfifo}[fx["runner"]]
+    ev = []
+    out, rep = runner(corpus, _RefVocabScorer(base, vocab), cfg, trace=True, on_step=ev.append)
+    oev = []
+    oref = {"run_varstream": O.run_varstream, "run_varbeam": O.run_varbeam,
+            "run_varfifo": O.run_varfifo}[fx["runner"]]
+    want, wrep = oref(corpus, _F32Rows(base), O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    assert [tuple(r) for r in rep.per_step_trace] == [tuple(r) for r in wrep.per_step_trace]
+    assert rep.simulated_cost == wrep.simulated_cost
+
+
+HASH_CASES = [
+    # name, V, k, n, M, delta, max_len, eps, N, dtype, scale, power, eos_bias
+    ("toy_c1", 1000, 5, 32, 3, 1.5, 48, 1 / 6, 160, "bf16", 8.0, 1, 6.0),
+    ("toy_fixed", 1000, 5, 32, 5, math.inf, 48, 1 / 6, 96, "f32", 8.0, 1, 6.0),
+    ("parse_c3", 2048, 10, 64, 3, 10.0, 40, 1 / 6, 120, "bf16", 6.0, 2, 5.0),
+    ("wide_k", 3000, 24, 8, 6, 2.0, 20, 1 / 4, 24, "f32", 10.0, 4, 9.0),
+]
+
+
+@pytest.mark.parametrize("case", HASH_CASES, ids=[c[0] for c in HASH_CASES])
+def test_device_hash_decode_matches_oracle(case):
+    """Whole VarStream decodes with the device scorer: every decision, event and
+    fp64 score bit-exact vs the oracle replaying the kernel's lse; the async
+    (sync-free) driver reproduces the synchronous one."""
+    name, V, k, n, M, delta, ml, eps, Nin, dt, scale, power, eb = case
+    P, N, SearchEngine, DeviceHashScorer, _, LseRecorder = _pkg()
+    vocab = P.Vocabulary(V, 0, 2)
+    cfg = P.DecodeConfig(k=k, n=n, epsilon=eps, delta=delta, max_candidates=M, max_len=ml)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(99, Nin, V, mean_len=8.0))
+    rec = LseRecorder(DeviceHashScorer(vocab, 5, scale=scale, power=power, eos_bias=eb, dtype=dt))
+    ev = []
+    out, rep = P.run_varstream(corpus, rec, cfg, trace=True, on_step=ev.append)
+    cpu = LseReplayScorer(HashLogitsCPU(V, 0, 2, 5, scale=scale, power=power, eos_bias=eb,
+                                        dtype=dt), rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    assert rep.candidate_expansions == wrep.candidate_expansions
+    # sync-free driver: identical outputs and counters
+    fast_out, fast_rep = P.run_varstream(
+        corpus, DeviceHashScorer(vocab, 5, scale=scale, power=power, eos_bias=eb, dtype=dt), cfg,
+        trace=True)
+    assert [[(c.tokens, c.score) for c in per] for per in fast_out] == O.signature(want)
+    assert fast_rep.per_step_trace == rep.per_step_trace
+
+
+def test_epsilon_and_scheduler_invariance_on_device():
+    """SPEC exactness/ε-independence (bb SPEC.md:379-380): outputs and expansion
+    totals identical across ε and across varstream/varbeam/varfifo."""
+    P, N, SearchEngine, DeviceHashScorer, *_ = _pkg()
+    vocab = P.Vocabulary(1000, 0, 2)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(4242, 300, 1000, mean_len=8.0))
+    sig = None
+    for runner, eps in ((P.run_varstream, 1 / 12), (P.run_varstream, 1 / 6), (P.run_varstream, 1 / 4),
+                        (P.run_varbeam, 1 / 6), (P.run_varfifo, 1 / 6)):
+        cfg = P.DecodeConfig(k=5, n=16, epsilon=eps, delta=1.5, max_candidates=3, max_len=48)
+        out, rep = runner(corpus, DeviceHashScorer(vocab, 31337, eos_bias=6.0), cfg)
+        s = ([[(c.tokens, c.score) for c in per] for per in out], rep.candidate_expansions)
+        sig = sig or s
+        assert s == sig
+
+
+def test_rows_copy_kernel():
+    P, N, *_ = _pkg()
+    lib = N.load_library()
+    planes, rows, maxpos, d = 3, 10, 6, 8
+    buf = torch.arange(planes * rows * maxpos * d, dtype=torch.float32, device="cuda").view(
+        planes, rows, maxpos, d)
+    ref = buf.clone()
+    cl = torch.tensor([1, 4, 3, 2, 7, 5], dtype=torch.int32, device="cuda")
+    nc = torch.tensor([2], dtype=torch.int32, device="cuda")
+    rc = lib.vs_rows_copy(buf.data_ptr(), buf.stride(0) * 4, planes, buf.stride(1) * 4, d * 4,
+                          cl.data_ptr(), nc.data_ptr(), 4, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref[:, 4, :3] = ref[:, 1, :3]
+    ref[:, 7, :5] = ref[:, 2, :5]
+    assert torch.equal(buf, ref)

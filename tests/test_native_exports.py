@@ -1,0 +1,98 @@
+"""CPU checks of the C-ABI library: it loads without a GPU and exports every
+symbol include/varstream.h declares; ctypes struct layouts match the header."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "varstream.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2010_02164_b200 import _native
+
+    if not _native.LIB_PATH.exists():
+        import __graft_entry__
+
+        __graft_entry__.build()
+    return _native.load_library()
+
+
+def header_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^int\s+(vs_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_bound_exports():
+    from paper_2010_02164_b200 import _native
+
+    assert header_functions() == sorted(_native.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert lib.vs_version() >= 1
+
+
+def test_struct_layouts_match_header():
+    from paper_2010_02164_b200 import _native
+
+    text = HEADER.read_text()
+    body = text[text.index("typedef struct vs_state"):text.index("} vs_state;")]
+    fields = re.findall(r"\*\s*(\w+);", body)
+    assert fields == _native.STATE_FIELDS
+    cfg = text[text.index("typedef struct vs_config"):text.index("} vs_config;")]
+    names = []
+    for decl in re.findall(r"(?:int32_t|double)\s+([\w, ]+);", cfg):
+        names += [x.strip() for x in decl.split(",")]
+    assert names == [f for f, _ in _native.VsConfig._fields_]
+    assert _native.VsConfig.delta.offset == 48 and C.sizeof(_native.VsConfig) == 56
+
+
+def test_host_argument_errors_map_to_reference_taxonomy(lib):
+    from paper_2010_02164_b200 import ConfigError, _native
+
+    rc = lib.vs_row_lse_topm(None, 0, 10, 10, 3, 1, None, 1, None, None, None, None, None)
+    assert rc == _native.VS_ERR_CONFIG
+    with pytest.raises(ConfigError):
+        _native.check(rc, "vs_row_lse_topm")
+
+
+def test_engine_refuses_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary
+    from paper_2010_02164_b200.engine import SearchEngine
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        SearchEngine(DecodeConfig(k=2, n=2), Vocabulary(10, 0, 1))
+
+
+def test_decode_config_validation_matches_reference():
+    import math
+
+    from paper_2010_02164_b200 import ConfigError, DecodeConfig
+
+    c = DecodeConfig(k=4, n=3)
+    assert c.max_candidates == 4 and c.capacity == 12 and c.delta == math.inf
+    for bad in (dict(k=0, n=1), dict(k=2, n=0), dict(k=2, n=1, epsilon=1.0),
+                dict(k=2, n=1, delta=-1.0), dict(k=2, n=1, max_candidates=3),
+                dict(k=2, n=1, max_len=1), dict(k=2, n=1, capacity=1),
+                dict(k=2, n=1, flush_interval=0), dict(k=2, n=1, cost_c0=0, cost_c1=0)):
+        with pytest.raises(ConfigError):
+            DecodeConfig(**bad)
+
+
+def test_metrics_rounding_goldens():
+    from goldens import load
+    from paper_2010_02164_b200 import MetricsReport
+
+    for row in load("metrics.json"):
+        r = MetricsReport(timesteps=row["steps"], candidate_expansions=row["expansions"])
+        assert r.summarize() == row["summary"]
