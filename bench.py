@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""VarStream search benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload wmt19_k50]
+    python bench.py --impl reference ...     # the reference algorithm on host cores
+
+A bench "step" is one complete ε-refill variable-width beam-search decode
+(run_varstream) of the workload's synthetic source batch.  The hot path per
+timestep is K3 schedule -> scorer logits -> K1 row_lse_topM -> K2 beam_step,
+all on device; the scorer is the deterministic device hash scorer standing in
+for the decoder's vocab projection (the decoder itself is SURVEY §8(f) row 1).
+
+value  = decoded sequences/s, whole job (all ranks), inputs resident in HBM.
+e2e    = same metric through the public API (run_varstream on host lists):
+         corpus H2D, decode, outputs D2H, all inside the timed region.
+roofline = K1 (the dominant search kernel): algorithmic bytes R_t*|V|*2 per
+         launch / CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # BASELINE.json configs[3]: WMT'19 transformer-big search shape
+    "wmt19_k50": dict(V=42024, sos=0, eos=2, k=50, n=128, M=5, delta=1.5, eps=1 / 6, max_len=256,
+                      N=10000, mean_len=25.0, clip=200, seed=99, scorer_seed=7, scale=0.5,
+                      power=0, eos_bias=7.5, dtype="bf16"),
+    # configs[0]/[1]: toy
+    "toy_c1": dict(V=1000, sos=0, eos=2, k=5, n=32, M=3, delta=1.5, eps=1 / 6, max_len=48, N=512,
+                   mean_len=8.0, clip=None, seed=4242, scorer_seed=31337, scale=0.5, power=0,
+                   eos_bias=5.0, dtype="bf16"),
+    # configs[2]: parsing shape
+    "parse_c3": dict(V=2048, sos=0, eos=2, k=10, n=256, M=3, delta=10.0, eps=1 / 6, max_len=64,
+                     N=20000, mean_len=12.0, clip=None, seed=99, scorer_seed=5, scale=0.5, power=0,
+                     eos_bias=5.5, dtype="bf16"),
+}
+METRIC = "decoded sequences/sec (ε-refill var-width beam, k=50); search-step HBM GB/s"
+
+
+def _corpus(w):
+    from paper_2010_02164_b200.harness import bucket_by_length, generate_synthetic_corpus
+
+    c = generate_synthetic_corpus(w["seed"], w["N"], w["V"], mean_len=w["mean_len"], clip=w["clip"])
+    return bucket_by_length(c)[0]
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- CPU reference
+def _cpu_worker(args):
+    """Runs in a spawned process: the oracle port of the reference search
+    (oracle/varstream_oracle.py, pinned to bb/scheduler.py run_varstream) with
+    the CPU mirror of the device scorer (fp64 log-softmax rows)."""
+    w, inputs = args
+    from oracle import varstream_oracle as O
+    from oracle.scorers import HashLogitsCPU
+
+    sc = HashLogitsCPU(w["V"], w["sos"], w["eos"], w["scorer_seed"], scale=w["scale"],
+                       power=w["power"], eos_bias=w["eos_bias"], dtype=w["dtype"])
+    cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"],
+                    max_candidates=w["M"], max_len=w["max_len"])
+    t0 = time.perf_counter()
+    _, rep = O.run_varstream(inputs, sc, cfg)
+    return time.perf_counter() - t0, rep.candidate_expansions
+
+
+def cpu_reference(w, corpus, per_proc: int, procs: int | None = None):
+    """Bounded sample (evenly strided over the length-sorted corpus), dealt to
+    `procs` single-threaded processes; returns (seq/s, cores, sample text)."""
+    import multiprocessing as mp
+
+    procs = procs or min(os.cpu_count() or 1, 64)
+    total = min(len(corpus), per_proc * procs)
+    stride = max(1, len(corpus) // total)
+    sample = corpus[::stride][:total]
+    shards = [sample[q::procs] for q in range(procs)]
+    shards = [s for s in shards if s]
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(shards)) as pool:
+        res = pool.map(_cpu_worker, [(w, s) for s in shards])
+    wall = time.perf_counter() - t0
+    busy = max(r[0] for r in res)
+    exp = sum(r[1] for r in res)
+    txt = (f"{total} of {len(corpus)} inputs (every {stride}th of the length-sorted corpus), "
+           f"{len(shards)} processes x 1 thread, {exp} expansions, slowest shard {busy:.1f}s")
+    return total / busy, len(shards), txt, wall
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ GPU bench
+def full_width_k1(w, iters: int = 20):
+    """K1 alone at the C4 full-width step (R = n*k rows x |V| bf16, 538 MB >
+    L2), L2 flushed between launches; CUDA events on the launch stream."""
+    import torch
+
+    from paper_2010_02164_b200.search import row_lse_topm
+
+    R = w["n"] * w["k"]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    # log-like logits (exponential upper tail, like the decode's scorer / real LMs)
+    u = torch.rand((R, w["V"]), device="cuda", generator=g).clamp_min_(2.0 ** -24)
+    x = (-w["scale"] * torch.log2(u)).to(torch.bfloat16)
+    del u
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    times = []
+    for i in range(iters + 3):
+        flush.fill_(i & 255)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        row_lse_topm(x, w["M"])
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.median(times)
+    _, _, _, fb = row_lse_topm(x, w["M"])
+    return R * w["V"] * 2, t, int(fb.item())
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
+    from paper_2010_02164_b200 import _native as N
+    from paper_2010_02164_b200.engine import SearchEngine
+    from paper_2010_02164_b200.harness import flatten, shard
+    from paper_2010_02164_b200.scorers import DeviceHashScorer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    w = WORKLOADS[args.workload]
+    if args.n_inputs:
+        w = dict(w, N=args.n_inputs)
+    corpus = _corpus(w)
+    mine = shard(len(corpus), world, rank)
+    local_corpus = [corpus[i] for i in mine]
+    vocab = Vocabulary(w["V"], w["sos"], w["eos"])
+    cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"],
+                       max_candidates=w["M"], max_len=w["max_len"])
+    scorer = DeviceHashScorer(vocab, w["scorer_seed"], scale=w["scale"], power=w["power"],
+                              eos_bias=w["eos_bias"], dtype=w["dtype"])
+    eng = SearchEngine(cfg, vocab)
+    tok, off = flatten(local_corpus)
+    d_tok, d_off = torch.from_numpy(tok).cuda(), torch.from_numpy(off).cuda()
+
+    def decode(k1=None):
+        _, rep = eng.run_async(None, scorer, admit_mode=N.VS_ADMIT_VARSTREAM,
+                               select_mode=N.VS_SELECT_MIN_LT, src_tok=d_tok, src_off=d_off,
+                               materialize=False, k1_events=k1)
+        return rep
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        decode()
+    k1 = []
+    reps = []
+    launches = 0
+    barrier()
+    with ClockSampler(local) as clocks:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            ev = []
+            reps.append(decode(ev))
+            launches += 5 * eng.launched_steps + 1
+            k1.extend(ev[: reps[-1].timesteps])
+        e1.record()
+        barrier()
+    t_local = e0.elapsed_time(e1) / 1e3
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    total_inputs = len(corpus) * args.steps
+    value = total_inputs / t_max
+    rep = reps[-1]
+    # K1 roofline: algorithmic bytes / event time, over the timed launches
+    k1_time = sum(a.elapsed_time(b) for a, b in k1) / 1e3
+    k1_bytes = sum(r.candidate_expansions for r in reps) * w["V"] * 2
+    peak, peak_kind = _peaks()
+    achieved = k1_bytes / k1_time / 1e9 if k1_time > 0 else 0.0
+    fb0 = int(eng.t["fallbacks"].item())
+    fw_bytes, fw_t, fw_fb = full_width_k1(w)
+    fw_gbs = fw_bytes / fw_t / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "k1_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+
+    # e2e through the public API: host lists in, Candidate lists out
+    e2e_t = []
+    for i in range(max(1, args.e2e_steps) + 1):
+        barrier()
+        s0 = time.perf_counter()
+        outs, _ = run_varstream(local_corpus, scorer, cfg)
+        ncand = sum(outs.count)  # DecodeResults holds the D2H copies
+        torch.cuda.synchronize()
+        if i:
+            e2e_t.append(time.perf_counter() - s0)
+    e2e_local = statistics.median(e2e_t)
+    te = torch.tensor([e2e_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = len(corpus) / float(te.item())
+    h2d = int(tok.nbytes + off.nbytes)
+    d2h = int(len(local_corpus) * 4 + len(local_corpus) * w["k"] * (4 + 8 + 4 * w["max_len"]))
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "seq/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "bf16 logits / fp32 lse / fp64 scores",
+        "data": "synthetic (reference generator bb/harness.py:85-115, seed %d; device hash scorer)" % w["seed"],
+        "config": {"workload": f"{args.workload}: |V|={w['V']} k={w['k']} n={w['n']} M={w['M']} "
+                               f"delta={w['delta']} eps=1/6 max_len={w['max_len']} N={len(corpus)}",
+                   "scorer": f"device hash scorer (log-like logits, scale {w['scale']}, eos_bias "
+                             f"{w['eos_bias']}) standing in for the decoder vocab projection",
+                   "global_batch": len(corpus), "batch_slots_n": w["n"], "parallelism": f"shard{world}",
+                   "l2": "not flushed inside the decode (producer->K1 reuse is part of the pipeline); "
+                         "roofline_full_width flushes L2 and uses 538 MB > L2",
+                   "timesteps_per_decode": rep.timesteps,
+                   "expansions_per_decode": rep.candidate_expansions,
+                   "expansions_per_step": round(rep.expansions_per_step, 1)},
+        "roofline": {"kernel": "vs_row_lse_topm (K1)", "bound": "hbm", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "bytes_per_launch": round(k1_bytes / max(1, len(k1))),
+                     "share_of_step": round(k1_time / t_max, 4),
+                     "exact_fallback_rows_total": fb0},
+        "roofline_full_width": {"kernel": "vs_row_lse_topm (K1)", "R": w["n"] * w["k"],
+                                "bytes": fw_bytes, "ms": round(fw_t * 1e3, 4),
+                                "achieved": round(fw_gbs, 1), "peak": peak, "unit": "GB/s",
+                                "frac": round(fw_gbs / peak, 4), "l2": "flushed (256 MB write)",
+                                "exact_fallback_rows": fw_fb},
+        "e2e": {"value": round(e2e_value, 2), "unit": "seq/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "paper_2010_02164_b200.run_varstream"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
+                                "sample": txt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    if args.n_inputs:
+        w = dict(w, N=args.n_inputs)
+    corpus = _corpus(w)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "seq/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None,
+        "dtype": "fp64 rows / fp64 scores", "data": "synthetic",
+        "config": {"workload": args.workload, "global_batch": w["N"]},
+        "cpu_baseline": {"value": round(value, 3), "unit": "seq/s", "cores": cores, "kind": "port",
+                         "sample": txt},
+        "e2e": {"value": round(value, 3), "unit": "seq/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="wmt19_k50")
+    ap.add_argument("--n-inputs", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-per-proc", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,14 +132,16 @@ class HashLogitsCPU:
     """Bit-exact CPU mirror of the device synthetic scorer's logits.
 
     logit[v] = scale * u^power, u = (fmix32(key ^ v*0x9E3779B9) >> 8) * 2^-24
-    (key folds the candidate's prefix hash), and
+    (key folds the candidate's prefix hash); power=0 is the log-like mode
+    logit = -scale * (e + f) for u' = u + 2^-24 = 2^e (1 + f) (a bit-cast log2,
+    exponential upper tail like real LM logits); and
     logit[eos] = (eos_bias * len) / src_len, all fp32 round-to-nearest; in
     bf16 mode each logit is then rounded to bf16.  Mirrors the structure of
     bb/model.py:209-218 with an integer hash in place of blake2b+PCG64."""
 
     def __init__(self, vocab_size: int, sos: int, eos: int, seed: int, *, scale: float = 8.0,
                  power: int = 1, eos_bias: float = 8.0, dtype: str = "f32"):
-        assert power in (1, 2, 4)
+        assert power in (0, 1, 2, 4)
         self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
         self.seed, self.scale, self.power = int(seed), np.float32(scale), power
         self.eos_bias, self.dtype = np.float32(eos_bias), dtype
@@ -155,12 +157,20 @@ class HashLogitsCPU:
         h = prefix_hash(enc.seed, tokens)
         key = np.uint32((h ^ (h >> 32)) & 0xFFFFFFFF)
         bits = fmix32_np(self._v ^ key)
-        u = (bits >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
-        if self.power >= 2:
-            u = u * u
-        if self.power >= 4:
-            u = u * u
-        x = (u * self.scale).astype(np.float32)
+        if self.power == 0:  # log-like: x = -scale * (e + f) with u = 2^e (1 + f)
+            b = (bits >> np.uint32(8)) + np.uint32(1)
+            u = b.astype(np.float32) * np.float32(2.0 ** -24)
+            ub = u.view(np.uint32)
+            e = (ub >> np.uint32(23)).astype(np.int32) - 127
+            f = (ub & np.uint32(0x7FFFFF)).astype(np.float32) * np.float32(2.0 ** -23)
+            x = (np.float32(-self.scale) * (e.astype(np.float32) + f)).astype(np.float32)
+        else:
+            u = (bits >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+            if self.power >= 2:
+                u = u * u
+            if self.power >= 4:
+                u = u * u
+            x = (u * self.scale).astype(np.float32)
         x[self.eos] = (self.eos_bias * np.float32(len(tokens))) / np.float32(enc.input_len)
         if self.dtype == "bf16":
             x = f32_to_bf16_rne(x)

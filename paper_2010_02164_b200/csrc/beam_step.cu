@@ -76,22 +76,44 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   int* emo = nfin + k;                              // [k] emission order -> child idx
   int* claimed = emo + k;                           // [k]
   int* inh = claimed + k;                           // [k]
+  __shared__ int wcnt[2][NT2 / 32];
   __shared__ int sh[8];  // 0 nact 1 nfin 2 nkept 3 nemit 4 first_remaining 5 emitted_after 6 next_width
 
+  // candidates -> smem (parallel loads; w <= k <= 128 = NT2)
   for (int i = tid; i < w; i += NT2) {
     cs[i] = st.c_score[base + i];
     ch[i] = st.c_hash[base + i];
     cl[i] = st.c_len[base + i];
     cr[i] = st.c_row[base + i];
   }
-  if (tid == 0) {
-    int na = 0, nf = 0;
-    for (int i = 0; i < w; ++i) {
-      if (st.c_fin[base + i]) fin[nf++] = i;
-      else act[na++] = i;
+  {  // stable split into finalized / active ordinals via warp ballots
+    const int lane = tid & 31, wid = tid >> 5;
+    const bool valid = tid < w;
+    const bool f = valid && st.c_fin[base + tid] != 0;
+    const unsigned bf = __ballot_sync(0xffffffffu, f);
+    const unsigned ba = __ballot_sync(0xffffffffu, valid && !f);
+    if (lane == 0) {
+      wcnt[0][wid] = __popc(bf);
+      wcnt[1][wid] = __popc(ba);
     }
-    sh[0] = na;
-    sh[1] = nf;
+    __syncthreads();
+    int fo = 0, ao = 0;
+    for (int q = 0; q < wid; ++q) {
+      fo += wcnt[0][q];
+      ao += wcnt[1][q];
+    }
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (f) fin[fo + __popc(bf & lt_mask)] = tid;
+    if (valid && !f) act[ao + __popc(ba & lt_mask)] = tid;
+    if (tid == 0) {
+      int na = 0, nf = 0;
+      for (int q = 0; q < NT2 / 32; ++q) {
+        nf += wcnt[0][q];
+        na += wcnt[1][q];
+      }
+      sh[0] = na;
+      sh[1] = nf;
+    }
   }
   __syncthreads();
   const int nact = sh[0], nfz = sh[1];

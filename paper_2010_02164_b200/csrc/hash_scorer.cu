@@ -27,6 +27,13 @@ __global__ void hash_encode_kernel(vs_config cfg, vs_state st, uint64_t seed) {
 
 __device__ __forceinline__ float hash_logit(uint32_t key, int v, float scale, int power) {
   const uint32_t bits = fmix32(((uint32_t)v * 0x9E3779B9u) ^ key);
+  if (power == 0) {  // log-like: -scale * (e + f), u' = ((bits>>8)+1) * 2^-24 = 2^e (1+f)
+    const float u1 = __fmul_rn((float)((bits >> 8) + 1u), 5.9604644775390625e-08f);
+    const uint32_t ub = __float_as_uint(u1);
+    const float e = (float)((int)(ub >> 23) - 127);
+    const float f = __fmul_rn((float)(ub & 0x7FFFFFu), 1.1920928955078125e-07f);
+    return __fmul_rn(-scale, __fadd_rn(e, f));
+  }
   float u = __fmul_rn((float)(bits >> 8), 5.9604644775390625e-08f);  // * 2^-24, exact
   if (power >= 2) u = __fmul_rn(u, u);
   if (power >= 4) u = __fmul_rn(u, u);
@@ -87,7 +94,7 @@ extern "C" int vs_hash_encode(const vs_config* cfg, const vs_state* st, uint64_t
 extern "C" int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs_hash_params* hp,
                               void* logits, int64_t ld, int32_t R_grid, void* stream) {
   if (!cfg || !st || !hp || !logits || ld < cfg->vocab_size) return VS_ERR_CONFIG;
-  if (hp->power != 1 && hp->power != 2 && hp->power != 4) return VS_ERR_CONFIG;
+  if (hp->power != 0 && hp->power != 1 && hp->power != 2 && hp->power != 4) return VS_ERR_CONFIG;
   if (R_grid <= 0) return VS_OK;
   if (R_grid > 65535) return VS_ERR_CONFIG;
   const int cols = (cfg->vocab_size + 8 * 256 - 1) / (8 * 256);

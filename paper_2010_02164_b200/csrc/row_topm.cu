@@ -4,67 +4,32 @@
 // bb/search.py:63-73 (_candidate_pool: first M of sorted(range(V),
 // key=(-row[t], t))), for every scored row of a timestep at once.
 //
-// One CTA per row.  The row is streamed from HBM exactly once with 16-byte
-// non-allocating vector loads (4 in flight per thread).  While streaming,
-// each thread keeps
-//   * an online (max, sum exp) pair                  -> lse
-//   * a sorted register list of its TL best logits   -> candidate superset
-// After a block-wide lse reduction every kept entry is re-keyed by the exact
-// contract value logp = fp32(x - lse) with token-ascending ties (a 64-bit
-// key), lists are merged by warp-shuffle argmax rounds (partial-sort merge)
-// and the block's top-M is verified: if any thread's TL-th kept entry could
-// still reach the M-th logp (ties/ambiguity), the row falls back to an exact
-// block radix select over 64-bit keys (re-reading the row).  Decisions never
-// depend on atomic ordering, so the result is a pure function of the row.
+// One WARP per row (4 independent warps per CTA, no block barriers).  The row
+// is read from HBM exactly once: 16-byte non-allocating vector loads, U
+// vectors per lane per batch, double-buffered so the next batch is in flight
+// while the current one is reduced.  Per element the hot loop does only the
+// online log-sum-exp (max, ex2, add) and one compare against a WARP-UNIFORM
+// candidate threshold θ (a 64-bit (logit, token) key):
+//   * θ is bootstrapped from a shuffle bitonic sort of the first batch's 32
+//     lane maxima (θ = M-th largest), so after the first batch only ~M·ln(V)
+//     elements ever pass the filter;
+//   * passing elements are appended to a per-warp shared-memory buffer with
+//     ballot/popc compaction; when it fills, M argmax rounds keep the top-M
+//     and raise θ (partial-sort merge).
+// Epilogue: warp-reduce lse, re-key the buffer by the contract value
+// logp = fp32(x - lse) with token-ascending ties, M warp-argmax rounds, and an
+// exact verification that no element filtered out by θ can reach the M-th
+// (logp, token) key — tie-aware, using the next-smaller representable input
+// value.  Rows that cannot be proven fall back to an exact warp radix select
+// over 64-bit keys.  Every decision is a pure function of the row.
 #include "common.cuh"
 
 namespace vs {
 namespace {
 
-template <int TL>
-__device__ __forceinline__ void list_insert(float (&lv)[TL], int (&lt)[TL], float x, int tok) {
-  float cv = x;
-  int ct = tok;
-#pragma unroll
-  for (int q = 0; q < TL; ++q) {
-    if (cv > lv[q]) {  // strict: equal logits keep the earlier (lower) token first
-      float tv = lv[q];
-      int tt = lt[q];
-      lv[q] = cv;
-      lt[q] = ct;
-      cv = tv;
-      ct = tt;
-    }
-  }
-}
-
-struct Online {
-  float m, s;
-};
-
-template <int TL, int N>
-__device__ __forceinline__ void consume(Online& o, float (&lv)[TL], int (&lt)[TL], const float (&x)[N],
-                                        int tok0) {
-  float cm = x[0];
-#pragma unroll
-  for (int j = 1; j < N; ++j) cm = fmaxf(cm, x[j]);
-  if (cm > o.m) {
-    o.s = (o.m == -INFINITY) ? 0.0f : o.s * exp2f((o.m - cm) * VS_LOG2E);
-    o.m = cm;
-  }
-  if (o.m != -INFINITY) {
-    const float ml = o.m * VS_LOG2E;
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      float e;
-      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(x[j], VS_LOG2E, -ml)));
-      o.s += e;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < N; ++j)
-    if (x[j] > lv[TL - 1]) list_insert<TL>(lv, lt, x[j], tok0 + j);
-}
+constexpr int WPC = 4;                 // warps per CTA (independent rows)
+constexpr int CAPW = 416;              // per-warp candidate buffer (keys)
+constexpr unsigned FULL = 0xffffffffu;
 
 template <typename T>
 __device__ __forceinline__ void unpack(const uint4& v, float (&x)[16 / sizeof(T)]);
@@ -87,203 +52,401 @@ __device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& v, float (&x)
   x[7] = bf16hi(v.w);
 }
 
-// Exact top-M by 64-bit key via MSB-first radix select (8 x 8-bit passes).
-// Rare path: only rows whose fast-path superset could not be proven.
-template <typename T, int NT>
-__device__ void exact_select(const T* __restrict__ row, int V, float lse, int Meff,
-                             uint64_t* __restrict__ out_keys, uint64_t* __restrict__ scratch,
-                             unsigned* __restrict__ hist) {
-  __shared__ uint64_t s_prefix;
-  __shared__ int s_want;
-  __shared__ unsigned s_cnt;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_prefix = 0;
-    s_want = Meff;
-    s_cnt = 0;
+// Next smaller value representable in the input dtype (for the tie-aware proof).
+template <typename T>
+__device__ __forceinline__ float prev_repr(float x);
+template <>
+__device__ __forceinline__ float prev_repr<float>(float x) {
+  return nextafterf(x, -INFINITY);
+}
+template <>
+__device__ __forceinline__ float prev_repr<__nv_bfloat16>(float x) {
+  const uint32_t u = __float_as_uint(x);
+  if (x == 0.0f) return __uint_as_float(0x80010000u);
+  if (isinf(x)) return x < 0.0f ? x : __uint_as_float(0x7f7f0000u);
+  return __uint_as_float((u & 0x80000000u) ? u + 0x10000u : u - 0x10000u);
+}
+
+// logit key: larger = earlier in (value desc, token asc).
+__device__ __forceinline__ uint64_t vkey(float x, int tok) {
+  return ((uint64_t)ord_f32(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)tok);
+}
+
+struct WarpState {
+  float m, s0, s1;    // online log-sum-exp (two partial sums)
+  uint64_t theta;     // candidate threshold key (warp-uniform); 0 = everything passes
+  float theta_x;      // logit part of theta (-inf when theta == 0)
+  int cnt;            // buffer fill (warp-uniform)
+};
+
+// Keep the top-`keep` keys of buf[0..cnt) in buf[0..keep) (sorted desc) using
+// `keep` warp-argmax rounds; returns the keep-th key (0 if fewer entries).
+__device__ __noinline__ uint64_t warp_select(uint64_t* __restrict__ buf, int cnt, int keep,
+                                             uint64_t* __restrict__ sel) {
+  const int lane = threadIdx.x & 31;
+  uint64_t last = 0;
+  for (int r = 0; r < keep; ++r) {
+    uint64_t lb = 0;
+    int li = -1;
+    for (int e = lane; e < cnt; e += 32) {
+      const uint64_t k = buf[e];
+      if (k > lb) {
+        lb = k;
+        li = e;
+      }
+    }
+    const uint64_t wb = warp_max_u64(lb);
+    if (wb != 0 && lb == wb) buf[li] = 0;  // unique owner (keys are distinct)
+    if (lane == 0) sel[r] = wb;
+    last = wb;
+    __syncwarp();
   }
-  __syncthreads();
+  for (int r = lane; r < keep; r += 32) buf[r] = sel[r];
+  __syncwarp();
+  return last;
+}
+
+// Exact fallback: M-th largest 64-bit (logp, token) key by MSB-first radix
+// select (8 x 8-bit passes over the row), then collect + rank the top-M.
+template <typename T>
+__device__ __noinline__ void warp_exact_select(const T* __restrict__ row, int V, float lse, int Meff,
+                                               unsigned* __restrict__ hist, uint64_t* __restrict__ buf,
+                                               uint64_t* __restrict__ sel) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0;
+  int want = Meff;
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
-    for (int i = tid; i < 256; i += NT) hist[i] = 0;
-    __syncthreads();
-    const uint64_t prefix = s_prefix;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
     const uint64_t hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
-    for (int i = tid; i < V; i += NT) {
+    for (int i = lane; i < V; i += 32) {
       const uint64_t key = row_key(__fsub_rn(to_f32<T>(row[i]), lse), i);
       if ((key & hi_mask) == (prefix & hi_mask)) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
-    __syncthreads();
-    if (tid == 0) {
-      int want = s_want;
+    __syncwarp();
+    int digit = 0, above = 0;
+    if (lane == 0) {
       unsigned cum = 0;
       for (int d = 255; d >= 0; --d) {
         const unsigned c = hist[d];
         if (cum + c >= (unsigned)want) {
-          s_want = want - (int)cum;
-          s_prefix = prefix | ((uint64_t)d << shift);
+          digit = d;
+          above = (int)cum;
           break;
         }
         cum += c;
       }
     }
-    __syncthreads();
+    digit = __shfl_sync(FULL, digit, 0);
+    above = __shfl_sync(FULL, above, 0);
+    want -= above;
+    prefix |= (uint64_t)digit << shift;
+    __syncwarp();
   }
-  const uint64_t kth = s_prefix;
-  for (int i = tid; i < V; i += NT) {
-    const uint64_t key = row_key(__fsub_rn(to_f32<T>(row[i]), lse), i);
-    if (key >= kth) {
-      const unsigned idx = atomicAdd(&s_cnt, 1u);
-      if (idx < (unsigned)VS_MAX_M) scratch[idx] = key;
+  int cnt = 0;  // exactly Meff keys are >= prefix (keys are unique)
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    uint64_t key = 0;
+    bool c = false;
+    if (i < V) {
+      key = row_key(__fsub_rn(to_f32<T>(row[i]), lse), i);
+      c = key >= prefix;
     }
+    const unsigned b = __ballot_sync(FULL, c);
+    if (c) buf[cnt + __popc(b & ((1u << lane) - 1u))] = key;
+    cnt += __popc(b);
   }
-  __syncthreads();
-  for (int j = tid; j < Meff; j += NT) {  // keys are unique -> ranks are a permutation
-    const uint64_t kj = scratch[j];
-    int rank = 0;
-    for (int i = 0; i < Meff; ++i) rank += scratch[i] > kj;
-    out_keys[rank] = kj;
-  }
-  __syncthreads();
+  __syncwarp();
+  warp_select(buf, cnt, Meff, sel);
 }
 
-template <typename T, int NT, int TL>
-__global__ void __launch_bounds__(NT) row_lse_topm_kernel(
+struct Cand {
+  uint64_t theta;  // candidate threshold key (warp-uniform); 0 = everything passes
+  float theta_x;   // logit part of theta (-inf when theta == 0)
+  int cnt;         // buffer fill (warp-uniform)
+};
+
+// Out-of-line candidate append (kept out of the hot loop's instruction
+// stream): a per-lane bitmask of elements >= θx, then one ballot round per
+// pending element (usually one round), keys compacted into the warp buffer.
+__device__ __noinline__ Cand append_slow(Cand c, float x0, float x1, float x2, float x3, float x4,
+                                         float x5, float x6, float x7, int n, int tok0,
+                                         uint64_t* __restrict__ buf, uint64_t* __restrict__ sel, int Meff,
+                                         int flush_at) {
+  const float x[8] = {x0, x1, x2, x3, x4, x5, x6, x7};
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned mask = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < n && x[j] >= c.theta_x) mask |= 1u << j;
+  while (__any_sync(FULL, mask != 0)) {
+    const int j = mask ? __ffs(mask) - 1 : 0;
+    float xj = x[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) xj = (j == q) ? x[q] : xj;
+    const uint64_t k = vkey(xj, tok0 + j);
+    const bool cnd = mask != 0 && k > c.theta;
+    mask &= mask - 1;
+    const unsigned b = __ballot_sync(FULL, cnd);
+    if (cnd) buf[c.cnt + __popc(b & lt_mask)] = k;
+    c.cnt += __popc(b);
+  }
+  if (c.cnt >= flush_at) {
+    __syncwarp();
+    c.theta = warp_select(buf, c.cnt, Meff, sel);
+    c.theta_x = unord_f32((uint32_t)(c.theta >> 32));
+    c.cnt = Meff;
+  }
+  return c;
+}
+
+struct PartSmem {  // per-warp results exchanged between the W warps of a row
+  float m, s;
+  uint64_t theta;
+  float theta_x;
+  int cnt;
+};
+
+// W warps per row (W in {1,2,4}; 4/W rows per CTA).  Warp `part` of a row
+// streams vectors [part*seg, (part+1)*seg); the row's leader warp combines.
+template <typename T, int U>
+__global__ void __launch_bounds__(WPC * 32, 5) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
-    int* __restrict__ fb_count, int normalized) {
-  constexpr int NW = NT / 32;
+    int* __restrict__ fb_count, int normalized, int sms) {
   constexpr int VEC = 16 / sizeof(T);
-  constexpr int U = 4;
-  __shared__ float red_m[NW], red_s[NW];
-  __shared__ uint64_t wkeys[NW][VS_MAX_M];
-  __shared__ uint64_t fkeys[VS_MAX_M];
-  __shared__ unsigned hist[256];
-  __shared__ float s_lse;
-
+  __shared__ uint64_t sbuf[WPC][CAPW];
+  __shared__ uint64_t ssel[WPC][VS_MAX_M];
+  __shared__ unsigned shist[WPC][256];
+  __shared__ PartSmem spart[WPC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = d_R ? *d_R : R_host;
-  const int r = blockIdx.x;
-  if (r >= R) return;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // warps per row from the live row count: enough warps for small steps, one
+  // warp per row once rows alone fill the machine
+  const int W = (V < 4096) ? 1 : (R < sms * 8 ? 4 : (R < sms * 16 ? 2 : 1));
+  const int part = wid % W, leader = wid - part;
+  const int r = blockIdx.x * (WPC / W) + wid / W;
+  if (blockIdx.x * (WPC / W) >= R) return;  // whole CTA idle (uniform)
+  const bool active = r < R;
+  uint64_t* buf = sbuf[wid];
+  uint64_t* sel = ssel[wid];
   const int Meff = M < V ? M : V;
-  const T* __restrict__ row = logits + (int64_t)r * ld;
+  const int flush_at = max(16, Meff + 8);
+  const T* __restrict__ row = logits + (int64_t)(active ? r : 0) * ld;
 
-  Online o{-INFINITY, 0.0f};
-  float lv[TL];
-  int lt[TL];
+  // m starts at a finite floor (logits must be > -1e30 or -inf) so the hot loop
+  // needs no -inf guards: ex2(x*log2e - m*log2e) is 0 for x = -inf and the
+  // branchless rescale ex2((m_old - m_new)*log2e) is 0 on the first vector.
+  constexpr float M_FLOOR = -1e30f;
+  float m = M_FLOOR, s0 = 0.0f, s1 = 0.0f;
+  Cand c{0ull, -INFINITY, 0};
+
+  auto consume = [&](const float (&x)[VEC], int n, int tok0) {
+    float cm = x[0];
 #pragma unroll
-  for (int q = 0; q < TL; ++q) {
-    lv[q] = -INFINITY;
-    lt[q] = 0x7fffffff;
-  }
+    for (int j = 1; j < VEC; ++j) cm = fmaxf(cm, x[j]);
+    const float mn = fmaxf(m, cm);
+    float sc;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(sc) : "f"((m - mn) * VS_LOG2E));
+    s0 *= sc;
+    s1 *= sc;
+    m = mn;
+    const float ml = m * VS_LOG2E;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      float e;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(x[j], VS_LOG2E, -ml)));
+      if (j & 1) s1 += e;
+      else s0 += e;
+    }
+    if (__any_sync(FULL, cm >= c.theta_x)) {
+      if (VEC == 8)
+        c = append_slow(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
+                        x[VEC > 6 ? 6 : 0], x[VEC > 7 ? 7 : 0], n, tok0, buf, sel, Meff, flush_at);
+      else
+        c = append_slow(c, x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
+                        -INFINITY, n, tok0, buf, sel, Meff, flush_at);
+    }
+  };
 
-  // ---- single streaming pass over the row ---------------------------------
-  int done = 0;
-  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-    const int nvec = V / VEC;
+  if (active) {
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
+    const int ntot = vec_ok ? V / VEC : 0;
+    const int seg = (ntot + W - 1) / W;
+    const int v0 = min(ntot, part * seg), v1 = min(ntot, v0 + seg);
     const uint4* __restrict__ vrow = reinterpret_cast<const uint4*>(row);
-    for (int b = tid; b < nvec; b += NT * U) {
-      uint4 v[U];
+    constexpr int BATCH = 32 * U;  // vectors per warp per batch
+    uint4 cur[U], nxt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = v0 + lane + 32 * u;
+      if (i < v1) cur[u] = ldg_stream(vrow + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = v0 + BATCH + lane + 32 * u;
+      if (i < v1) nxt[u] = ldg_stream(vrow + i);
+    }
+    if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 batches
+      float lm = -INFINITY;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = b + u * NT;
-        if (i < nvec) v[u] = ldg_stream(vrow + i);
+        float x[VEC];
+        if (v0 + lane + 32 * u < v1) {
+          unpack<T>(cur[u], x);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+        }
+        if (v0 + BATCH + lane + 32 * u < v1) {
+          unpack<T>(nxt[u], x);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+        }
+      }
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const float o = __shfl_xor_sync(FULL, lm, j);
+          lm = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(lm, o) : fminf(lm, o);
+        }
+      const float t0 = __shfl_sync(FULL, lm, Meff - 1);
+      if (t0 != -INFINITY) {
+        c.theta = (uint64_t)ord_f32(t0) << 32;  // (t0, token = +inf): x == t0 still passes
+        c.theta_x = t0;
+      }
+    }
+    int base = v0;
+    // full double-batches: no per-vector bounds checks
+    for (; base + 2 * BATCH <= v1; base += 2 * BATCH) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float x[VEC];
+        unpack<T>(cur[u], x);
+        consume(x, VEC, (base + lane + 32 * u) * VEC);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = b + u * NT;
-        if (i < nvec) {
+        const int i = base + 2 * BATCH + lane + 32 * u;
+        if (i < v1) cur[u] = ldg_stream(vrow + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float x[VEC];
+        unpack<T>(nxt[u], x);
+        consume(x, VEC, (base + BATCH + lane + 32 * u) * VEC);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + 3 * BATCH + lane + 32 * u;
+        if (i < v1) nxt[u] = ldg_stream(vrow + i);
+      }
+    }
+    // remainder (< 2 batches, already loaded into cur / nxt): checked
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + h * BATCH + lane + 32 * u;
+        if (__any_sync(FULL, i < v1)) {
           float x[VEC];
-          unpack<T>(v[u], x);
-          consume<TL, VEC>(o, lv, lt, x, i * VEC);
+          if (i < v1) unpack<T>(h ? nxt[u] : cur[u], x);
+          else
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) x[j] = -INFINITY;
+          consume(x, VEC, i * VEC);
         }
       }
     }
-    done = nvec * VEC;
-  }
-  for (int i = done + tid; i < V; i += NT) {  // tail (or unaligned row)
-    float x[1] = {to_f32<T>(row[i])};
-    consume<TL, 1>(o, lv, lt, x, i);
-  }
-
-  // ---- lse = max + log(sum exp(x - max)) ---------------------------------------
+    if (part == W - 1) {  // tail / unaligned rows
+      for (int i0 = ntot * VEC; i0 < V; i0 += 32) {
+        const int i = i0 + lane;
+        float x[VEC];
+        x[0] = i < V ? to_f32<T>(row[i]) : -INFINITY;
 #pragma unroll
-  for (int m = 16; m > 0; m >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, o.m, m);
-    const float s2 = __shfl_xor_sync(0xffffffffu, o.s, m);
-    lse_merge(o.m, o.s, m2, s2);
-  }
-  if (lane == 0) {
-    red_m[wid] = o.m;
-    red_s[wid] = o.s;
-  }
-  __syncthreads();
-  if (wid == 0) {
-    float mm = lane < NW ? red_m[lane] : -INFINITY;
-    float ss = lane < NW ? red_s[lane] : 0.0f;
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, mm, m);
-      const float s2 = __shfl_xor_sync(0xffffffffu, ss, m);
-      lse_merge(mm, ss, m2, s2);
-    }
-    if (lane == 0) s_lse = (mm == -INFINITY) ? -INFINITY : mm + logf(ss);
-  }
-  __syncthreads();
-  const float lse = normalized ? 0.0f : s_lse;
-
-  // ---- exact keys, per-thread sort ---------------------------------------------
-  uint64_t key[TL];
-#pragma unroll
-  for (int q = 0; q < TL; ++q) key[q] = (lt[q] == 0x7fffffff) ? 0ull : row_key(__fsub_rn(lv[q], lse), lt[q]);
-#pragma unroll
-  for (int i = 0; i < TL; ++i)
-#pragma unroll
-    for (int j = 0; j < TL - 1 - i; ++j)
-      if (key[j] < key[j + 1]) {
-        const uint64_t t = key[j];
-        key[j] = key[j + 1];
-        key[j + 1] = t;
+        for (int j = 1; j < VEC; ++j) x[j] = -INFINITY;
+        consume(x, 1, i);
       }
-
-  // ---- warp merge: Meff argmax rounds over lane heads -------------------------
-  for (int j = 0; j < Meff; ++j) {
-    const uint64_t best = warp_max_u64(key[0]);
-    if (best != 0ull && key[0] == best) {
+    }
+  }
+  // ---- per-warp lse partial -> exchange --------------------------------------------
+  float s = s0 + s1;
 #pragma unroll
-      for (int q = 0; q < TL - 1; ++q) key[q] = key[q + 1];
-      key[TL - 1] = 0ull;
-    }
-    if (lane == 0) wkeys[wid][j] = best;
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(FULL, m, o);
+    const float s2 = __shfl_xor_sync(FULL, s, o);
+    lse_merge(m, s, m2, s2);
   }
-  __syncthreads();
-  // ---- block merge of NW sorted warp lists (warp 0) ---------------------------
-  if (wid == 0) {
-    int pos = 0;
-    uint64_t head = lane < NW ? wkeys[lane][0] : 0ull;
-    for (int j = 0; j < Meff; ++j) {
-      const uint64_t best = warp_max_u64(head);
-      if (best != 0ull && head == best) {
-        ++pos;
-        head = pos < Meff ? wkeys[lane][pos] : 0ull;
+  if (W > 1) {
+    if (lane == 0) {
+      spart[wid].m = m;
+      spart[wid].s = s;
+    }
+    __syncthreads();
+    m = -INFINITY;
+    s = 0.0f;
+    for (int q = 0; q < W; ++q) lse_merge(m, s, spart[leader + q].m, spart[leader + q].s);
+  }
+  const float lse_raw = (m <= -1e30f || s == 0.0f) ? -INFINITY : m + logf(s);
+  const float lse = normalized ? 0.0f : lse_raw;
+  // ---- re-key own candidates by (logp, token) ---------------------------------------
+  __syncwarp();
+  for (int e = lane; e < c.cnt; e += 32) {
+    const uint64_t k = buf[e];
+    buf[e] = row_key(__fsub_rn(unord_f32((uint32_t)(k >> 32)), lse), (int)(0xffffffffu - (uint32_t)k));
+  }
+  if (W > 1) {
+    if (lane == 0) {
+      spart[wid].theta = c.theta;
+      spart[wid].theta_x = c.theta_x;
+      spart[wid].cnt = c.cnt;
+    }
+    __syncthreads();
+    if (part != 0 || !active) return;
+    // leader: gather the other parts' candidates behind its own (CAPW suffices:
+    // each part holds < flush_at + 256 entries only transiently; after the
+    // stream it holds < flush_at <= 160, and W <= 4 parts -> keep top-Meff each)
+    for (int q = 1; q < W; ++q) {
+      const int nq = spart[leader + q].cnt;
+      const uint64_t* bq = sbuf[leader + q];
+      if (c.cnt + nq > CAPW) {  // compact own buffer first (exact: by final key)
+        __syncwarp();
+        warp_select(buf, c.cnt, Meff, sel);
+        c.cnt = Meff;
       }
-      if (lane == 0) fkeys[j] = best;
+      for (int e = lane; e < nq; e += 32) buf[c.cnt + e] = bq[e];
+      c.cnt += nq;
+      __syncwarp();
     }
   }
-  __syncthreads();
-
-  // ---- verification: can a rejected entry reach the M-th logp? ----------------
-  const uint64_t kth = fkeys[Meff - 1];
-  int fail = (kth == 0ull);
-  if (!fail) fail = ord_f32(__fsub_rn(lv[TL - 1], lse)) >= (uint32_t)(kth >> 32);
-  if (__syncthreads_or(fail)) {
-    exact_select<T, NT>(row, V, lse, Meff, fkeys, &wkeys[0][0], hist);
-    if (tid == 0 && fb_count) atomicAdd(fb_count, 1);
+  if (!active) return;
+  __syncwarp();
+  const uint64_t kth = c.cnt >= Meff ? warp_select(buf, c.cnt, Meff, sel) : 0ull;
+  // ---- proof that nothing filtered out by any part's θ precedes the M-th key -----
+  bool ok = kth != 0ull;
+  for (int q = 0; q < W && ok; ++q) {
+    const uint64_t th = W > 1 ? spart[leader + q].theta : c.theta;
+    const float tx = W > 1 ? spart[leader + q].theta_x : c.theta_x;
+    if (th == 0ull) continue;  // that part kept every element it saw
+    const uint32_t t_lp = (uint32_t)(kth >> 32);
+    const int t_tok = key_tok(kth);
+    const int th_tok = (int)(0xffffffffu - (uint32_t)th);  // -1 encodes "+inf token"
+    // (a) values strictly below θ's logit: their logp <= fl(prev(θx) - lse)
+    ok = ord_f32(__fsub_rn(prev_repr<T>(tx), lse)) < t_lp;
+    // (b) values equal to θ's logit with a larger token than θ's
+    if (ok) {
+      const uint32_t lp = ord_f32(__fsub_rn(tx, lse));
+      ok = lp < t_lp || (lp == t_lp && (th_tok == -1 || th_tok >= t_tok));
+    }
   }
-
-  for (int j = tid; j < M; j += NT) {
+  if (!ok) {
+    warp_exact_select<T>(row, V, lse, Meff, shist[wid], buf, sel);
+    if (lane == 0 && fb_count) atomicAdd(fb_count, 1);
+  }
+  for (int j = lane; j < M; j += 32) {
     if (j < Meff) {
-      const uint64_t kk = fkeys[j];
+      const uint64_t kk = sel[j];
       top_tok[(int64_t)r * M + j] = key_tok(kk);
       top_logp[(int64_t)r * M + j] = key_logp(kk);
     } else {
@@ -291,35 +454,32 @@ __global__ void __launch_bounds__(NT) row_lse_topm_kernel(
       top_logp[(int64_t)r * M + j] = -INFINITY;
     }
   }
-  if (tid == 0 && row_lse) row_lse[r] = lse;
-}
-
-template <typename T, int NT>
-int launch_tl(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int grid,
-              int* top_tok, float* top_logp, float* row_lse, int* fb, int norm, cudaStream_t st) {
-  const T* p = static_cast<const T*>(logits);
-  const int TLsel = M <= 4 ? M : (M <= 16 ? 4 : 8);
-  switch (TLsel) {
-    case 1: row_lse_topm_kernel<T, NT, 1><<<grid, NT, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm); break;
-    case 2: row_lse_topm_kernel<T, NT, 2><<<grid, NT, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm); break;
-    case 3: row_lse_topm_kernel<T, NT, 3><<<grid, NT, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm); break;
-    case 4: row_lse_topm_kernel<T, NT, 4><<<grid, NT, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm); break;
-    default: row_lse_topm_kernel<T, NT, 8><<<grid, NT, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm); break;
-  }
-  VS_CUDA_RET();
+  if (lane == 0 && row_lse) row_lse[r] = lse;
 }
 
 template <typename T>
-int launch_nt(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int grid,
-              int* top_tok, float* top_logp, float* row_lse, int* fb, int norm, cudaStream_t st) {
-  if (V >= 8192) return launch_tl<T, 256>(logits, ld, V, M, R_host, d_R, grid, top_tok, top_logp, row_lse, fb, norm, st);
-  return launch_tl<T, 128>(logits, ld, V, M, R_host, d_R, grid, top_tok, top_logp, row_lse, fb, norm, st);
+int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int rows, int* top_tok,
+           float* top_logp, float* row_lse, int* fb, int norm, cudaStream_t st) {
+  // warps per row: enough warps in flight for small steps (>= ~2 rows' worth per
+  // SM-quarter), one warp per row once rows alone fill the machine.
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // grid covers the worst case over the W the kernel will pick from the live R
+  const int grid = max((rows + WPC - 1) / WPC, V >= 4096 ? min(rows, sms * 8) : 0);
+  const T* p = static_cast<const T*>(logits);
+  row_lse_topm_warp_kernel<T, 4><<<grid, WPC * 32, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp,
+                                                            row_lse, fb, norm, sms);
+  VS_CUDA_RET();
 }
 
 }  // namespace
 }  // namespace vs
 
-extern "C" int vs_version(void) { return 1; }
+extern "C" int vs_version(void) { return 2; }
 
 extern "C" int vs_row_lse_topm(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
                                int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,
@@ -332,8 +492,8 @@ extern "C" int vs_row_lse_topm(const void* logits, int32_t dtype, int64_t ld, in
   const int norm = (dtype & VS_ROWS_NORMALIZED) ? 1 : 0;
   dtype &= ~VS_ROWS_NORMALIZED;
   if (dtype == VS_DTYPE_F32)
-    return vs::launch_nt<float>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse, fallback_count, norm, st);
+    return vs::launch<float>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse, fallback_count, norm, st);
   if (dtype == VS_DTYPE_BF16)
-    return vs::launch_nt<__nv_bfloat16>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse, fallback_count, norm, st);
+    return vs::launch<__nv_bfloat16>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse, fallback_count, norm, st);
   return VS_ERR_CONFIG;
 }

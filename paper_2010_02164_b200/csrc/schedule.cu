@@ -84,14 +84,18 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
 
   // ---- A. removal of finished beams (stable) ------------------------------------
   if (do_remove && !first) {
-    if (tid == 0) {
+    {  // finished ids in selection order (bb/scheduler.py:186-189), parallel
       const int nsel_prev = status[VS_ST_NSEL];
-      int nf = 0;
-      for (int b = 0; b < nsel_prev; ++b) {
-        const int s = st.sel[b];
-        if (st.slot_flags[s] & 2) stat_fin[nf++] = st.slot_input[s];
+      int f = 0, fin_input = 0;
+      if (tid < nsel_prev) {
+        const int s = st.sel[tid];
+        f = (st.slot_flags[s] & 2) != 0;
+        if (f) fin_input = st.slot_input[s];
       }
-      sh[0] = nf;
+      int tot;
+      const int p = block_excl_scan(f, wsum, &tot);
+      if (f) stat_fin[p] = fin_input;
+      if (tid == 0) sh[0] = tot;
     }
     int s = -1, keep = 0;
     if (tid < n_live) {
@@ -250,20 +254,30 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
   if (n_live == 0) eff = 0;
 
   // ---- D. row list: active candidates of each selected beam, beam order ------------
-  if (tid < nsel) {
-    const int s = st.sel[tid];
-    int r = st.sel_off[tid];
-    const int width = st.slot_width[s];
-    for (int j = 0; j < width; ++j) {
-      const int c = s * k + j;
-      if (st.c_fin[c]) continue;
-      st.row_slot[r] = s;
-      st.row_cand[r] = j;
-      st.row_phys[r] = s * k + st.c_row[c];
-      st.row_len[r] = st.c_len[c];
-      ++r;
+  // one warp per selected beam: ballot-compact its active candidates (beam order)
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int b = wid; b < nsel; b += NT3 / 32) {
+      const int s = st.sel[b];
+      const int r0 = st.sel_off[b];
+      const int width = st.slot_width[s];
+      int before = 0;
+      for (int j0 = 0; j0 < width; j0 += 32) {
+        const int j = j0 + lane;
+        const int c = s * k + j;
+        const bool act = j < width && !st.c_fin[c];
+        const unsigned m = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          const int r = r0 + before + __popc(m & ((1u << lane) - 1u));
+          st.row_slot[r] = s;
+          st.row_cand[r] = j;
+          st.row_phys[r] = s * k + st.c_row[c];
+          st.row_len[r] = st.c_len[c];
+        }
+        before += __popc(m);
+      }
+      if (lane == 0) stat_sel[b] = st.slot_input[s];
     }
-    stat_sel[tid] = st.slot_input[s];
   }
   if (tid < n_live) st.live[tid] = live_s[tid];
   if (tid == 0) {

@@ -156,10 +156,12 @@ class SearchEngine:
         self.t["src_tok"] = (src_tok if src_tok.numel() else torch.zeros(1, dtype=torch.int32)).to(
             dev, non_blocking=True)
         k, L = self.k, self.max_len
-        self.t["out_count"] = torch.zeros(n_in, dtype=torch.int32, device=dev)
-        self.t["out_len"] = torch.zeros(n_in * k, dtype=torch.int32, device=dev)
-        self.t["out_score"] = torch.zeros(n_in * k, dtype=torch.float64, device=dev)
-        self.t["out_tok"] = torch.zeros(n_in * k * L, dtype=torch.int32, device=dev)
+        if self.t.get("out_count") is None or self.t["out_count"].shape[0] != n_in:
+            # only entries the beam step emits are ever read; admission zeroes counts
+            self.t["out_count"] = torch.zeros(n_in, dtype=torch.int32, device=dev)
+            self.t["out_len"] = torch.empty(n_in * k, dtype=torch.int32, device=dev)
+            self.t["out_score"] = torch.empty(n_in * k, dtype=torch.float64, device=dev)
+            self.t["out_tok"] = torch.empty(n_in * k * L, dtype=torch.int32, device=dev)
         for f in ("src_off", "src_tok", "out_count", "out_len", "out_score", "out_tok"):
             setattr(self.state, f, self.t[f].data_ptr())
 
@@ -276,7 +278,7 @@ class SearchEngine:
 
     def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
                   ring: int = 8, trace: bool = False, src_tok=None, src_off=None,
-                  materialize: bool = True):
+                  materialize: bool = True, k1_events: list | None = None):
         """Host-sync-free driver (no flush / no StepEvents): every kernel reads
         R_t from device memory, status headers are streamed into a pinned ring
         and consumed `ring` steps behind the device."""
@@ -309,11 +311,18 @@ class SearchEngine:
             events[slot].record(stream)
             scorer.on_admit(self, None)
             logits, code = scorer.logits(self, None)
+            if k1_events is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
             self.row_topm(logits, code, 0, cap, d_R)
+            if k1_events is not None:
+                e1.record(stream)
+                k1_events.append((e0, e1))
             self.beam_step()
             scorer.after_step(self, None)
             self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
             launched += 1
+        self.launched_steps = launched
         st = self.read_status()
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
