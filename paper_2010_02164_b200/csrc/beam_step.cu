@@ -1,5 +1,7 @@
 // K2 beam_step: per-beam merge, δ/M pruning, EOS finalisation, emission,
-// length-cap drain and row planning (sm_100a).  One CTA per selected beam.
+// length-cap drain and row planning (sm_100a).  One CTA (128 threads) per
+// selected beam; every phase is data-parallel (no single-thread loops over
+// candidates), so the critical path is a handful of barriers.
 //
 // Restates, for the deferred policy (bb/core.py:18-28):
 //   _candidate_pool   bb/search.py:52-73   (no-ops + per-parent top-M, fp64 add)
@@ -10,27 +12,35 @@
 //   advance_beam      bb/search.py:215-230 + _drain_at_length_cap :190-202
 //   beam_finished     bb/search.py:205-212
 //
+// Selection: the pool is w sorted lists (one per finalized candidate — its
+// no-op — and one per active parent — its M proposals, K1's order re-checked
+// against (score desc, token asc)).  An entry's rank is the sum over lists of
+// how many of their entries precede it, counted from each list head; entries
+// below kept[0].score - delta are never ranked.  The per-parent cap never
+// binds (each parent contributes min(M, V) proposals, all accepted by
+// max_candidates_filter), so kept = the first min(k, |pool|) entries at or
+// above the δ cutoff.
+//
 // Row planning (new, no reference equivalent): candidates are logical; each
 // owns a physical row of the slot (token history + scorer row state such as
 // a KV cache).  The first child of a parent inherits the parent's row (no
-// copy); further children take rows freed by parents without surviving
-// children and get a (src,dst,len) copy entry.  Sources are always rows
-// claimed by inheritors, destinations always free rows, so in-place copies
-// are hazard-free.
-//
-// The per-parent cap never binds here: each parent contributes exactly
-// min(M, V) proposals (pre-truncated by K1), so max_candidates_filter accepts
-// every extension and the kept set is the first min(k, |pool|) in order.
+// copy); further children take the rows left free, in ascending order, and
+// get a (src,dst,len) copy entry.  Sources are always rows claimed by
+// inheritors, destinations always free rows, so in-place copies are
+// hazard-free.
 #include "common.cuh"
 
 namespace vs {
 namespace {
 
-struct PoolView {
+constexpr int NT2 = 128;  // == VS_MAX_K: one thread per candidate / child
+constexpr unsigned FULLM = 0xffffffffu;
+
+struct Pool {
   const double* sc;
   const int* par;
   const int* tok;
-  // true when entry f precedes e in proposal_order (score desc, parent asc, token asc)
+  // entry f precedes e in proposal_order (score desc, parent asc, token asc)
   __device__ __forceinline__ bool before(int f, int e) const {
     const double a = sc[f], b = sc[e];
     if (a != b) return a > b;
@@ -39,13 +49,28 @@ struct PoolView {
   }
 };
 
-constexpr int NT2 = 128;
+// Block-wide (NT2 threads) exclusive prefix count of a predicate.
+__device__ __forceinline__ int block_prefix(bool pred, int* wsm, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(FULLM, pred);
+  if (lane == 0) wsm[wid] = __popc(b);
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < NT2 / 32; ++q) {
+    off += q < wid ? wsm[q] : 0;
+    tot += wsm[q];
+  }
+  __syncthreads();
+  *total = tot;
+  return off + __popc(b & ((1u << lane) - 1u));
+}
 
 __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.x;
   if (b >= st.status[VS_ST_NSEL]) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int k = cfg.k;
   const int s = st.sel[b];
   const int L = st.slot_lt[s];
@@ -56,70 +81,54 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   const int Pmax = k + k * Meff;
 
   // ---- shared memory carve-up -------------------------------------------------
-  double* cs = reinterpret_cast<double*>(smem);  // [k]  current scores
-  uint64_t* ch = reinterpret_cast<uint64_t*>(cs + k);  // [k]
-  double* ps = reinterpret_cast<double*>(ch + k);  // [Pmax] pool score
-  double* ns = ps + Pmax;                           // [k] child score
-  uint64_t* nh = reinterpret_cast<uint64_t*>(ns + k);  // [k] child hash
-  int* pp = reinterpret_cast<int*>(nh + k);         // [Pmax] pool parent
-  int* pt = pp + Pmax;                              // [Pmax] pool token (-1 = no-op)
-  int* cl = pt + Pmax;                              // [k] current len
-  int* cr = cl + k;                                 // [k] current row
-  int* act = cr + k;                                // [k] active ordinal -> cand idx
-  int* fin = act + k;                               // [k] finalized ordinal -> cand idx
-  int* kept = fin + k;                              // [k] pool index by rank
-  int* nrow = kept + k;                             // [k] child row
-  int* nsrc = nrow + k;                             // [k] copy source row (-1 none)
-  int* nlen = nsrc + k;                             // [k] child len
-  int* ntok = nlen + k;                             // [k] appended token (-1 none)
-  int* nfin = ntok + k;                             // [k] child finalized
-  int* emo = nfin + k;                              // [k] emission order -> child idx
-  int* claimed = emo + k;                           // [k]
-  int* inh = claimed + k;                           // [k]
-  __shared__ int wcnt[2][NT2 / 32];
-  __shared__ int sh[8];  // 0 nact 1 nfin 2 nkept 3 nemit 4 first_remaining 5 emitted_after 6 next_width
+  double* cs = reinterpret_cast<double*>(smem);       // [k] current scores
+  uint64_t* ch = reinterpret_cast<uint64_t*>(cs + k);  // [k] current hashes
+  double* ps = reinterpret_cast<double*>(ch + k);     // [Pmax] pool score
+  int* pp = reinterpret_cast<int*>(ps + Pmax);        // [Pmax] pool parent
+  int* pt = pp + Pmax;                                // [Pmax] pool token (-1 = no-op)
+  int* cl = pt + Pmax;                                // [k] current len
+  int* cr = cl + k;                                   // [k] current row
+  int* act = cr + k;                                  // [k] active ordinal -> cand idx
+  int* fin = act + k;                                 // [k] finalized ordinal -> cand idx
+  int* kept = fin + k;                                // [k] pool index by rank
+  int* firstc = kept + k;                             // [k] first child of parent (atomicMin)
+  int* claimed = firstc + k;                          // [k] row claimed
+  int* freel = claimed + k;                           // [k] free rows, ascending
+  int* emo = freel + k;                               // [k] emission order -> child
+  int* nrow = emo + k;                                // [k] child row
+  int* csrc = nrow + k;                               // [k] child copy source row (-1)
+  int* nlen = csrc + k;                               // [k] child length
+  __shared__ int wsm[NT2 / 32];
+  __shared__ int s_kept;
+  __shared__ double s_cut;
 
-  // candidates -> smem (parallel loads; w <= k <= 128 = NT2)
-  for (int i = tid; i < w; i += NT2) {
-    cs[i] = st.c_score[base + i];
-    ch[i] = st.c_hash[base + i];
-    cl[i] = st.c_len[base + i];
-    cr[i] = st.c_row[base + i];
+  // ---- candidates -> smem; stable finalized / active split ---------------------
+  bool isfin = false;
+  if (tid < w) {
+    cs[tid] = st.c_score[base + tid];
+    ch[tid] = st.c_hash[base + tid];
+    cl[tid] = st.c_len[base + tid];
+    cr[tid] = st.c_row[base + tid];
+    isfin = st.c_fin[base + tid] != 0;
   }
-  {  // stable split into finalized / active ordinals via warp ballots
-    const int lane = tid & 31, wid = tid >> 5;
-    const bool valid = tid < w;
-    const bool f = valid && st.c_fin[base + tid] != 0;
-    const unsigned bf = __ballot_sync(0xffffffffu, f);
-    const unsigned ba = __ballot_sync(0xffffffffu, valid && !f);
-    if (lane == 0) {
-      wcnt[0][wid] = __popc(bf);
-      wcnt[1][wid] = __popc(ba);
-    }
-    __syncthreads();
-    int fo = 0, ao = 0;
-    for (int q = 0; q < wid; ++q) {
-      fo += wcnt[0][q];
-      ao += wcnt[1][q];
-    }
-    const unsigned lt_mask = (1u << lane) - 1u;
-    if (f) fin[fo + __popc(bf & lt_mask)] = tid;
-    if (valid && !f) act[ao + __popc(ba & lt_mask)] = tid;
-    if (tid == 0) {
-      int na = 0, nf = 0;
-      for (int q = 0; q < NT2 / 32; ++q) {
-        nf += wcnt[0][q];
-        na += wcnt[1][q];
-      }
-      sh[0] = na;
-      sh[1] = nf;
+  if (tid < k) {
+    firstc[tid] = 0x7fffffff;
+    claimed[tid] = 0;
+  }
+  if (tid == 0) s_kept = 0;
+  int nfz, nact;
+  {
+    const int fpos = block_prefix(tid < w && isfin, wsm, &nfz);
+    const int apos = block_prefix(tid < w && !isfin, wsm, &nact);
+    if (tid < w) {
+      if (isfin) fin[fpos] = tid;
+      else act[apos] = tid;
     }
   }
   __syncthreads();
-  const int nact = sh[0], nfz = sh[1];
   const int P = nfz + nact * Meff;
 
-  // ---- pool (bb/search.py:64-72): no-ops then per-parent top-M ------------------
+  // ---- pool (bb/search.py:64-72): no-ops, then per-parent top-M ----------------
   for (int e = tid; e < P; e += NT2) {
     if (e < nfz) {
       const int i = fin[e];
@@ -136,149 +145,191 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
     }
   }
   __syncthreads();
-
-  // ---- first min(k, P) in proposal_order: exact rank counting with early exit ----
-  // Scan order visits no-ops then every parent's best proposals first, so
-  // entries outside the top-k stop after ~k comparisons.
+  // per-parent lists sorted by (score desc, token asc); equal fp64 sums of
+  // distinct logps may reorder K1's (logp desc, token asc) output (rare).
+  for (int a = tid; a < nact; a += NT2) {
+    const int b0 = nfz + a * Meff;
+    bool sorted = true;
+    for (int m = 0; m + 1 < Meff; ++m)
+      if (ps[b0 + m] < ps[b0 + m + 1] || (ps[b0 + m] == ps[b0 + m + 1] && pt[b0 + m] > pt[b0 + m + 1]))
+        sorted = false;
+    if (!sorted)
+      for (int m = 1; m < Meff; ++m) {
+        const double sv = ps[b0 + m];
+        const int tv = pt[b0 + m];
+        int q = m - 1;
+        while (q >= 0 && (ps[b0 + q] < sv || (ps[b0 + q] == sv && pt[b0 + q] > tv))) {
+          ps[b0 + q + 1] = ps[b0 + q];
+          pt[b0 + q + 1] = pt[b0 + q];
+          --q;
+        }
+        ps[b0 + q + 1] = sv;
+        pt[b0 + q + 1] = tv;
+      }
+  }
+  __syncthreads();
+  const Pool pool{ps, pp, pt};
+  const int NL = nfz + nact;  // == w lists
+  // ---- rank-0 entry = best list head (warp 0) -> δ cutoff ------------------------
+  if (wid == 0) {
+    int best = -1;
+    for (int Lh = lane; Lh < NL; Lh += 32) {
+      const int e = Lh < nfz ? Lh : nfz + (Lh - nfz) * Meff;
+      if (best < 0 || pool.before(e, best)) best = e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int other = __shfl_xor_sync(FULLM, best, o);
+      if (other >= 0 && (best < 0 || pool.before(other, best))) best = other;
+    }
+    if (lane == 0) s_cut = (cfg.delta != INFINITY && best >= 0) ? ps[best] - cfg.delta : -INFINITY;
+  }
+  __syncthreads();
+  const double cutoff = s_cut;
+  // ---- ranks of entries at/above the cutoff --------------------------------------
   const int kk = P < k ? P : k;
-  const PoolView pv{ps, pp, pt};
+  int mine = 0;
   for (int e = tid; e < P; e += NT2) {
+    if (!(ps[e] >= cutoff)) continue;  // pruned by the absolute threshold (inclusive)
     int rank = 0;
-    for (int j = 0; j < P && rank < kk; ++j) {
-      int f;
-      if (j < nfz) f = j;
-      else {
-        const int jj = j - nfz, m = jj / nact, a = jj - m * nact;
-        f = nfz + a * Meff + m;
-      }
-      rank += pv.before(f, e);
+    for (int Lh = 0; Lh < NL && rank < kk; ++Lh) {
+      const int b0 = Lh < nfz ? Lh : nfz + (Lh - nfz) * Meff;
+      const int len = Lh < nfz ? 1 : Meff;
+      for (int q = 0; q < len && pool.before(b0 + q, e); ++q) ++rank;  // list is sorted
     }
-    if (rank < kk) kept[rank] = e;
+    if (rank < kk) {
+      kept[rank] = e;
+      ++mine;
+    }
+  }
+  if (mine) atomicAdd(&s_kept, mine);
+  __syncthreads();
+  const int nkept = s_kept;  // ranks 0..nkept-1 are filled (contiguous prefix)
+
+  // ---- materialise children (thread j = child j) --------------------------------
+  const int j = tid;
+  const bool child = j < nkept;
+  int pi = 0, tk = -1, clen = 0, crow = 0, src = -1, cfin = 0;
+  double csc = 0.0;
+  uint64_t chh = 0;
+  if (child) {
+    const int e = kept[j];
+    pi = pp[e];
+    tk = pt[e];
+    csc = ps[e];
+    if (tk < 0) {  // no-op: the finalized candidate itself (bb/search.py:114-115)
+      chh = ch[pi];
+      clen = cl[pi];
+      cfin = 1;
+      crow = cr[pi];
+      claimed[crow] = 1;
+    } else {
+      chh = prefix_step(ch[pi], tk);
+      clen = cl[pi] + 1;
+      cfin = (tk == cfg.eos) || (cl[pi] + 1 >= cfg.max_len);  // bb/core.py:174
+      atomicMin(&firstc[pi], j);
+    }
   }
   __syncthreads();
-
-  // ---- threshold, materialisation, row plan, emission, drain (one thread) ------
-  if (tid == 0) {
-    int nk = kk;
-    if (cfg.delta != INFINITY) {  // bb/heuristics.py:75-78, anchor = kept[0]
-      const double cutoff = ps[kept[0]] - cfg.delta;
-      int j = 0;
-      while (j < nk && ps[kept[j]] >= cutoff) ++j;
-      nk = j;
+  bool extra = false;
+  if (child && tk >= 0) {
+    if (firstc[pi] == j) {  // the parent's first child inherits its row
+      crow = cr[pi];
+      claimed[crow] = 1;
+    } else {
+      extra = true;
+      src = cr[pi];
     }
-    for (int r = 0; r < k; ++r) {
-      claimed[r] = 0;
-      inh[r] = 0;
-    }
-    for (int j = 0; j < nk; ++j) {
-      const int e = kept[j], i = pp[e], t = pt[e];
-      ns[j] = ps[e];
-      if (t < 0) {  // no-op: the finalized candidate itself
-        nh[j] = ch[i];
-        nlen[j] = cl[i];
-        ntok[j] = -1;
-        nfin[j] = 1;
-        nrow[j] = cr[i];
-        nsrc[j] = -1;
-        claimed[cr[i]] = 1;
-      } else {
-        nh[j] = prefix_step(ch[i], t);
-        nlen[j] = cl[i] + 1;
-        ntok[j] = t;
-        nfin[j] = (t == cfg.eos) || (cl[i] + 1 >= cfg.max_len);  // bb/core.py:174
-        if (!inh[i]) {
-          inh[i] = 1;
-          nrow[j] = cr[i];
-          nsrc[j] = -1;
-          claimed[cr[i]] = 1;
-        } else {
-          nrow[j] = -1;
-          nsrc[j] = cr[i];
-        }
+  }
+  __syncthreads();
+  {
+    int nfree, nextra;
+    const bool fr = tid < k && !claimed[tid];
+    const int fpos = block_prefix(fr, wsm, &nfree);
+    if (fr) freel[fpos] = tid;
+    const int xpos = block_prefix(extra, wsm, &nextra);  // barrier inside orders freel
+    if (extra) crow = freel[xpos];
+  }
+  if (child) {
+    nrow[j] = crow;
+    csrc[j] = src;
+    nlen[j] = clen;
+  }
+  // ---- deferred emission + length-cap drain ------------------------------------
+  const int emitted0 = st.slot_emitted[s];
+  int first, ne, width;
+  {
+    const unsigned bnf = __ballot_sync(FULLM, child && !cfin);
+    if (lane == 0) wsm[wid] = bnf ? wid * 32 + __ffs(bnf) - 1 : 0x7fffffff;
+    __syncthreads();
+    int nlead = nkept;  // leading finalized children
+    for (int q = 0; q < NT2 / 32; ++q) nlead = min(nlead, wsm[q]);
+    __syncthreads();
+    first = min(nlead, k - emitted0);  // pops, bb/search.py:139-141
+    ne = first;
+    if (child && j < first) emo[j] = j;
+    width = nkept - first;
+    if (!cfg.no_drain && L + 1 >= cfg.max_len && width > 0) {  // bb/search.py:227-229, :190-202
+      const bool rem = child && j >= first;
+      int nf_rem, nn_rem;
+      const int fpos = block_prefix(rem && cfin, wsm, &nf_rem);
+      const int npos = block_prefix(rem && !cfin, wsm, &nn_rem);
+      const int quota = k - emitted0 - first;
+      if (rem) {
+        const int pos = cfin ? fpos : nf_rem + npos;  // finalized first, then capped
+        if (pos < quota) emo[first + pos] = j;
       }
-    }
-    int fr = 0;
-    for (int j = 0; j < nk; ++j) {
-      if (nrow[j] >= 0) continue;
-      while (claimed[fr]) ++fr;
-      nrow[j] = fr;
-      claimed[fr] = 1;
-    }
-    // deferred emission: pop rank-1 finalized while emitted < k (bb/search.py:139-141)
-    int emitted = st.slot_emitted[s];
-    int ne = 0, first = 0;
-    while (first < nk && nfin[first] && emitted < k) {
-      emo[ne++] = first++;
-      ++emitted;
-    }
-    int width = nk - first;
-    // length-cap drain (bb/search.py:227-229, :190-202): finalized, then capped
-    if (!cfg.no_drain && L + 1 >= cfg.max_len && width > 0) {
-      for (int pass = 0; pass < 2; ++pass)
-        for (int j = first; j < nk; ++j) {
-          if ((pass == 0) != (nfin[j] != 0)) continue;
-          if (emitted >= k) break;
-          emo[ne++] = j;
-          ++emitted;
-        }
+      ne = first + min(quota, nf_rem + nn_rem);
       width = 0;
-      first = nk;
     }
-    sh[2] = nk;
-    sh[3] = ne;
-    sh[4] = first;
-    sh[5] = emitted;
-    sh[6] = width;
   }
   __syncthreads();
-  const int nk = sh[2], ne = sh[3], first = sh[4], width = sh[6];
+  // ---- token histories: copy parent prefixes into new rows (warp per child) ----
   const int ML = cfg.max_len;
-
-  // ---- token histories: copy parent prefix into new rows, then append -------
-  for (int j = 0; j < nk; ++j) {
-    if (nsrc[j] < 0) continue;
-    const int32_t* src = st.hist + (int64_t)(base + nsrc[j]) * ML;
-    int32_t* dst = st.hist + (int64_t)(base + nrow[j]) * ML;
-    for (int p = tid; p < L; p += NT2) dst[p] = src[p];
+  for (int c = wid; c < nkept; c += NT2 / 32) {
+    const int sr = csrc[c];
+    if (sr < 0) continue;
+    const int32_t* srcp = st.hist + (int64_t)(base + sr) * ML;
+    int32_t* dstp = st.hist + (int64_t)(base + nrow[c]) * ML;
+    for (int p = lane; p < L; p += 32) dstp[p] = srcp[p];
   }
   __syncthreads();
-  for (int j = tid; j < nk; j += NT2)
-    if (ntok[j] >= 0) st.hist[(int64_t)(base + nrow[j]) * ML + L] = ntok[j];
+  if (child && tk >= 0) st.hist[(int64_t)(base + crow) * ML + L] = tk;
   __syncthreads();
 
-  // ---- emission into the per-input output buffers ----------------------------
+  // ---- emission into the per-input output buffers (warp per emission) ---------
   const int input = st.slot_input[s];
-  const int e0 = st.slot_emitted[s];
-  for (int q = 0; q < ne; ++q) {
-    const int j = emo[q];
-    const int64_t o = (int64_t)input * k + e0 + q;
-    const int32_t* src = st.hist + (int64_t)(base + nrow[j]) * ML;
-    for (int p = tid; p < nlen[j]; p += NT2) st.out_tok[o * ML + p] = src[p];
-    if (tid == 0) {
-      st.out_len[o] = nlen[j];
-      st.out_score[o] = ns[j];
+  for (int q = wid; q < ne; q += NT2 / 32) {
+    const int c = emo[q];
+    const int64_t o = (int64_t)input * k + emitted0 + q;
+    const int32_t* srcp = st.hist + (int64_t)(base + nrow[c]) * ML;
+    const int len = nlen[c];
+    for (int p = lane; p < len; p += 32) st.out_tok[o * ML + p] = srcp[p];
+    if (lane == 0) {
+      st.out_len[o] = len;
+      st.out_score[o] = ps[kept[c]];
     }
   }
 
   // ---- next beam SoA, KV copy plan, slot state ---------------------------------
-  for (int j = tid; j < width; j += NT2) {
-    const int c = first + j;
-    st.c_score[base + j] = ns[c];
-    st.c_hash[base + j] = nh[c];
-    st.c_len[base + j] = nlen[c];
-    st.c_row[base + j] = nrow[c];
-    st.c_fin[base + j] = (uint8_t)nfin[c];
-    if (nsrc[c] >= 0 && !nfin[c]) {  // only active children are scored again
+  const bool stays = child && j >= first && j < first + width;
+  if (stays) {
+    const int d = j - first;
+    st.c_score[base + d] = csc;
+    st.c_hash[base + d] = chh;
+    st.c_len[base + d] = clen;
+    st.c_row[base + d] = crow;
+    st.c_fin[base + d] = (uint8_t)cfin;
+    if (src >= 0 && !cfin) {  // only active children are scored again
       const int slot = atomicAdd(st.n_copy, 1);
-      st.copy_list[3 * slot + 0] = base + nsrc[c];
-      st.copy_list[3 * slot + 1] = base + nrow[c];
+      st.copy_list[3 * slot + 0] = base + src;
+      st.copy_list[3 * slot + 1] = base + crow;
       st.copy_list[3 * slot + 2] = L;
     }
   }
+  const int nact2 = __syncthreads_count(stays && !cfin);
   if (tid == 0) {
-    int nact2 = 0;
-    for (int j = first; j < first + width; ++j) nact2 += !nfin[j];
-    const int emitted = sh[5];
+    const int emitted = emitted0 + ne;
     st.slot_width[s] = width;
     st.slot_active[s] = nact2;
     st.slot_lt[s] = L + 1;
@@ -301,8 +352,7 @@ extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
   const int Meff = cfg->max_candidates < cfg->vocab_size ? cfg->max_candidates : cfg->vocab_size;
   if (M_rows < Meff) return VS_ERR_CONFIG;
   const int Pmax = k + k * Meff;
-  const size_t smem = (size_t)(4 * k + Pmax) * 8 /*cs,ch,ns,nh + ps*/ + (size_t)2 * Pmax * 4 +
-                      (size_t)15 * k * 4 + 64;
+  const size_t smem = (size_t)(2 * k + Pmax) * 8 + (size_t)2 * Pmax * 4 + (size_t)13 * k * 4 + 64;
   if (smem > 200 * 1024) return VS_ERR_CONFIG;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {

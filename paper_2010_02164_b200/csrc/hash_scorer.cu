@@ -47,37 +47,42 @@ __device__ __forceinline__ float cvt<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
-// grid: (chunks of 8*NT columns, rows); 8 consecutive tokens per thread.
+// Persistent grid-stride over (row, 2048-column chunk) work items with the
+// live row count read from device memory: no empty CTAs are launched for
+// rows beyond R_t.  8 consecutive tokens per thread, one 16-byte store (bf16).
 template <typename T>
 __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_state st, vs_hash_params hp,
-                                                          T* __restrict__ logits, int64_t ld) {
-  const int r = blockIdx.y;
-  if (r >= st.status[VS_ST_R]) return;
+                                                          T* __restrict__ logits, int64_t ld, int cols) {
+  const int R = st.status[VS_ST_R];
   const int V = cfg.vocab_size;
-  const int v0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (v0 >= V) return;
-  const int s = st.row_slot[r];
-  const uint64_t h = st.c_hash[s * cfg.k + st.row_cand[r]];
-  const uint32_t key = (uint32_t)(h ^ (h >> 32));
-  const float eos_val = __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
-  T* out = logits + (int64_t)r * ld;
-  T vals[8];
+  for (int w = blockIdx.x; w < R * cols; w += gridDim.x) {
+    const int r = w / cols, cchunk = w - r * cols;
+    const int v0 = (cchunk * blockDim.x + threadIdx.x) * 8;
+    if (v0 >= V) continue;
+    const int s = st.row_slot[r];
+    const uint64_t h = st.c_hash[s * cfg.k + st.row_cand[r]];
+    const uint32_t key = (uint32_t)(h ^ (h >> 32));
+    const float eos_val =
+        __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
+    T* out = logits + (int64_t)r * ld;
+    T vals[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int v = v0 + j;
-    const float x = (v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power);
-    vals[j] = cvt<T>(x);
-  }
-  const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
-  if (vec_ok) {
-    if (sizeof(T) == 2) {
-      *reinterpret_cast<uint4*>(out + v0) = *reinterpret_cast<const uint4*>(vals);
-    } else {
-      reinterpret_cast<uint4*>(out + v0)[0] = reinterpret_cast<const uint4*>(vals)[0];
-      reinterpret_cast<uint4*>(out + v0)[1] = reinterpret_cast<const uint4*>(vals)[1];
+    for (int j = 0; j < 8; ++j) {
+      const int v = v0 + j;
+      const float x = (v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power);
+      vals[j] = cvt<T>(x);
     }
-  } else {
-    for (int j = 0; j < 8 && v0 + j < V; ++j) out[v0 + j] = vals[j];
+    const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
+    if (vec_ok) {
+      if (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(out + v0) = *reinterpret_cast<const uint4*>(vals);
+      } else {
+        reinterpret_cast<uint4*>(out + v0)[0] = reinterpret_cast<const uint4*>(vals)[0];
+        reinterpret_cast<uint4*>(out + v0)[1] = reinterpret_cast<const uint4*>(vals)[1];
+      }
+    } else {
+      for (int j = 0; j < 8 && v0 + j < V; ++j) out[v0 + j] = vals[j];
+    }
   }
 }
 
@@ -96,14 +101,20 @@ extern "C" int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs
   if (!cfg || !st || !hp || !logits || ld < cfg->vocab_size) return VS_ERR_CONFIG;
   if (hp->power != 0 && hp->power != 1 && hp->power != 2 && hp->power != 4) return VS_ERR_CONFIG;
   if (R_grid <= 0) return VS_OK;
-  if (R_grid > 65535) return VS_ERR_CONFIG;
   const int cols = (cfg->vocab_size + 8 * 256 - 1) / (8 * 256);
-  dim3 grid(cols, R_grid);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long need = (long)R_grid * cols;
+  const int grid = (int)(need < (long)sms * 8 ? need : (long)sms * 8);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (hp->dtype == VS_DTYPE_F32)
-    vs::hash_logits_kernel<float><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<float*>(logits), ld);
+    vs::hash_logits_kernel<float><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<float*>(logits), ld, cols);
   else if (hp->dtype == VS_DTYPE_BF16)
-    vs::hash_logits_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<__nv_bfloat16*>(logits), ld);
+    vs::hash_logits_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<__nv_bfloat16*>(logits), ld, cols);
   else
     return VS_ERR_CONFIG;
   VS_CUDA_RET();

@@ -1,6 +1,6 @@
 // K3 compact_refill_select: the VarStream scheduler step on device (sm_100a).
 //
-// One CTA (1024 threads, one live-list entry per thread) per call:
+// One CTA (1024 threads, one slot / live-list entry per thread) per call:
 //   A. stable removal of finished beams      bb/scheduler.py:190-192 (+ finished
 //      ids in selection order :186-189 for StepEvent)
 //   B. ε-refill at the top of the step        bb/scheduler.py:94-116, :237-240,
@@ -11,8 +11,10 @@
 //      ConfigError :125-128)
 //   D. the next step's row list: active candidates of the selected beams in
 //      beam order (bb/search.py:223-225)
-// Slots never move: the live list is an index list and admission takes the
-// lowest free slot ids (physical placement does not affect results).
+// All per-slot state is pulled into shared memory in one round of independent
+// loads, so the kernel costs ~3 dependent global round trips.  Slots never
+// move: the live list is an index list and admission takes the lowest free
+// slot ids (physical placement does not affect results).
 #include "common.cuh"
 
 namespace vs {
@@ -49,12 +51,25 @@ __device__ int block_excl_scan(int v, int* warp_sums, int* tot) {
   return res;
 }
 
+__device__ __forceinline__ int block_min(int v, int* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int m = 0x7fffffff;
+  for (int q = 0; q < NT3 / 32; ++q) m = min(m, scratch[q]);
+  __syncthreads();
+  return m;
+}
+
 __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state st, int N, int first,
                                                        int do_remove, int admit_mode, int select_mode) {
   __shared__ int wsum[33];
   __shared__ int live_s[VS_MAX_SLOTS];
   __shared__ int order_s[VS_MAX_SLOTS];
-  __shared__ int sh[16];
+  __shared__ int flags_s[VS_MAX_SLOTS], lt_s[VS_MAX_SLOTS], act_s[VS_MAX_SLOTS], input_s[VS_MAX_SLOTS];
+  __shared__ int width_s[VS_MAX_SLOTS], off_s[VS_MAX_SLOTS + 1];
+  __shared__ int sh[8];
   const int tid = threadIdx.x;
   const int n = cfg.n, k = cfg.k;
   int32_t* status = st.status;
@@ -63,57 +78,52 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
   int32_t* stat_live = stat_fin + n;
   int32_t* stat_adm = stat_live + n;
 
-  if (first) {
-    for (int s = tid; s < n; s += NT3) st.slot_flags[s] = 0;
-    if (tid == 0) {
-      st.counters[0] = 0;
-      st.counters[1] = 0;
-      st.counters[2] = N;
-      status[VS_ST_NSEL] = 0;
-    }
-    __syncthreads();
-  }
-  int n_live = st.counters[0];
-  int cursor = st.counters[1];
-  if (tid < n_live) live_s[tid] = st.live[tid];
-  if (tid == 0) {
-    sh[0] = 0;  // nfin
-    sh[1] = 0;  // error
+  // ---- one round of independent loads -------------------------------------------
+  int n_live = first ? 0 : st.counters[0];
+  int cursor = first ? 0 : st.counters[1];
+  const int nsel_prev = first ? 0 : status[VS_ST_NSEL];
+  int prev_sel = -1;
+  if (tid < n) {
+    flags_s[tid] = first ? 0 : st.slot_flags[tid];
+    lt_s[tid] = st.slot_lt[tid];
+    act_s[tid] = st.slot_active[tid];
+    width_s[tid] = st.slot_width[tid];
+    input_s[tid] = st.slot_input[tid];
+    live_s[tid] = st.live[tid];
+    prev_sel = st.sel[tid];
   }
   __syncthreads();
 
   // ---- A. removal of finished beams (stable) ------------------------------------
+  int nfin = 0;
   if (do_remove && !first) {
-    {  // finished ids in selection order (bb/scheduler.py:186-189), parallel
-      const int nsel_prev = status[VS_ST_NSEL];
+    {  // finished ids in selection order (bb/scheduler.py:186-189)
       int f = 0, fin_input = 0;
       if (tid < nsel_prev) {
-        const int s = st.sel[tid];
-        f = (st.slot_flags[s] & 2) != 0;
-        if (f) fin_input = st.slot_input[s];
+        f = (flags_s[prev_sel] & 2) != 0;
+        if (f) fin_input = input_s[prev_sel];
       }
       int tot;
       const int p = block_excl_scan(f, wsum, &tot);
       if (f) stat_fin[p] = fin_input;
-      if (tid == 0) sh[0] = tot;
+      nfin = tot;
     }
     int s = -1, keep = 0;
     if (tid < n_live) {
       s = live_s[tid];
-      keep = !(st.slot_flags[s] & 2);
+      keep = !(flags_s[s] & 2);
     }
     int tot;
     const int pos = block_excl_scan(keep, wsum, &tot);
-    __syncthreads();
     if (tid < n_live) {
       if (keep) live_s[pos] = s;
-      else st.slot_flags[s] = 0;  // slot freed
+      else flags_s[s] = 0;  // slot freed
     }
     n_live = tot;
     __syncthreads();
   }
   const int n_live_after = n_live;
-  if (tid < n_live_after) stat_live[tid] = st.slot_input[live_s[tid]];
+  if (tid < n_live_after) stat_live[tid] = input_s[live_s[tid]];
 
   // ---- B. refill ------------------------------------------------------------------------
   int n_admit = 0;
@@ -126,17 +136,20 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
   }
   if (admit) {
     n_admit = min(n - n_live, N - cursor);
-    int is_free = 0, s = tid;
-    if (tid < n) is_free = !(st.slot_flags[s] & 1);
+    const int is_free = tid < n && !(flags_s[tid] & 1);
     int tot;
     const int fpos = block_excl_scan(is_free, wsum, &tot);
     if (is_free && fpos < n_admit) {
-      const int input = cursor + fpos;
+      const int s = tid, input = cursor + fpos;
       live_s[n_live + fpos] = s;
       stat_adm[fpos] = s;
-      st.slot_flags[s] = 1;
+      flags_s[s] = 1;
+      input_s[s] = input;
+      lt_s[s] = 1;  // Beam.initial, bb/core.py:79-82
+      act_s[s] = 1;
+      width_s[s] = 1;
       st.slot_input[s] = input;
-      st.slot_lt[s] = 1;  // Beam.initial, bb/core.py:79-82
+      st.slot_lt[s] = 1;
       st.slot_emitted[s] = 0;
       st.slot_width[s] = 1;
       st.slot_active[s] = 1;
@@ -153,30 +166,18 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
     cursor += n_admit;
     __syncthreads();
   }
+  if (tid < n) st.slot_flags[tid] = flags_s[tid];
 
   // ---- C. selection -------------------------------------------------------------------
-  // candidate list in advance order -> order_s[0..nc)
-  int nc = 0;
-  int eff = 0;
+  int nc = 0, eff = 0;
   if (n_live > 0) {
-    int lt = 0, s = -1;
+    int lt = 0x7fffffff, s = -1;
     if (tid < n_live) {
       s = live_s[tid];
-      lt = st.slot_lt[s];
+      lt = lt_s[s];
     }
     if (select_mode == VS_SELECT_MIN_LT) {
-      int mn = tid < n_live ? lt : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      if ((tid & 31) == 0) order_s[tid >> 5] = mn;
-      __syncthreads();
-      if (tid == 0) {
-        int m = 0x7fffffff;
-        for (int wv = 0; wv < NT3 / 32; ++wv) m = min(m, order_s[wv]);
-        sh[2] = m;
-      }
-      __syncthreads();
-      eff = sh[2];
+      eff = block_min(lt, wsum);
       const int in_front = tid < n_live && lt == eff;
       int tot;
       const int p = block_excl_scan(in_front, wsum, &tot);
@@ -185,9 +186,9 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
     } else if (select_mode == VS_SELECT_FIFO) {  // sort by (-l_t, arrival)
       if (tid < n_live) {
         int rank = 0;
-        for (int j = 0; j < n_live; ++j) {
-          const int lj = st.slot_lt[live_s[j]];
-          rank += (lj > lt) || (lj == lt && j < tid);
+        for (int q = 0; q < n_live; ++q) {
+          const int lq = lt_s[live_s[q]];
+          rank += (lq > lt) || (lq == lt && q < tid);
         }
         order_s[rank] = s;
       }
@@ -200,30 +201,30 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
   }
 
   // pack (bb/scheduler.py:119-132): fast path when everything fits
-  int w = 0;
-  if (tid < nc) w = st.slot_active[order_s[tid]];
+  const int wdt = tid < nc ? act_s[order_s[tid]] : 0;
   int tot_w;
-  const int wpos = block_excl_scan(w, wsum, &tot_w);
+  const int wpos = block_excl_scan(wdt, wsum, &tot_w);
   int nsel = 0, R = 0;
-  int bad = __syncthreads_or(tid < nc && w > cfg.capacity);
-  if (bad) {
-    if (tid == 0) sh[1] = VS_ERR_CONFIG;
-  } else if (tot_w <= cfg.capacity) {
+  const int bad = __syncthreads_or(tid < nc && wdt > cfg.capacity);
+  if (!bad && tot_w <= cfg.capacity) {
     if (tid < nc) {
       st.sel[tid] = order_s[tid];
       st.sel_off[tid] = wpos;
+      off_s[tid] = wpos;
     }
     nsel = nc;
     R = tot_w;
-  } else {
+  } else if (!bad) {
     if (tid == 0) {
       int total = 0, c = 0;
       for (int i = 0; i < nc; ++i) {
         const int s = order_s[i];
-        const int wi = st.slot_active[s];
+        const int wi = act_s[s];
         if (total + wi <= cfg.capacity) {
+          order_s[c] = s;  // in place: c <= i
           st.sel[c] = s;
           st.sel_off[c] = total;
+          off_s[c] = total;
           ++c;
           total += wi;
         }
@@ -236,47 +237,79 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
     R = sh[4];
   }
   if (tid == 0) st.sel_off[nsel] = R;
-  __syncthreads();
-  if (select_mode != VS_SELECT_MIN_LT && nsel > 0) {  // effective_len = max l_t of chosen
-    int lt = tid < nsel ? st.slot_lt[st.sel[tid]] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lt = max(lt, __shfl_xor_sync(0xffffffffu, lt, o));
-    if ((tid & 31) == 0) wsum[tid >> 5] = lt;
-    __syncthreads();
-    if (tid == 0) {
-      int m = 0;
-      for (int wv = 0; wv < NT3 / 32; ++wv) m = max(m, wsum[wv]);
-      sh[5] = m;
-    }
-    __syncthreads();
-    eff = sh[5];
-  }
+  if (select_mode != VS_SELECT_MIN_LT && nsel > 0)  // effective_len = max l_t of chosen
+    eff = -block_min(tid < nsel ? -lt_s[order_s[tid]] : 0x7fffffff, wsum);
   if (n_live == 0) eff = 0;
 
   // ---- D. row list: active candidates of each selected beam, beam order ------------
-  // one warp per selected beam: ballot-compact its active candidates (beam order)
+  // one warp per selected beam; a warp's (<= 4 beams) x (<= 2 chunks of 32)
+  // candidate loads are issued together so the phase costs one round trip.
+  __syncthreads();
   {
     const int lane = tid & 31, wid = tid >> 5;
-    for (int b = wid; b < nsel; b += NT3 / 32) {
-      const int s = st.sel[b];
-      const int r0 = st.sel_off[b];
-      const int width = st.slot_width[s];
-      int before = 0;
-      for (int j0 = 0; j0 < width; j0 += 32) {
-        const int j = j0 + lane;
-        const int c = s * k + j;
-        const bool act = j < width && !st.c_fin[c];
-        const unsigned m = __ballot_sync(0xffffffffu, act);
-        if (act) {
-          const int r = r0 + before + __popc(m & ((1u << lane) - 1u));
-          st.row_slot[r] = s;
-          st.row_cand[r] = j;
-          st.row_phys[r] = s * k + st.c_row[c];
-          st.row_len[r] = st.c_len[c];
+    constexpr int NB = VS_MAX_SLOTS / (NT3 / 32) > 4 ? 4 : VS_MAX_SLOTS / (NT3 / 32);
+    if (k <= 64 && nsel <= NB * (NT3 / 32)) {
+      unsigned char fz[NB][2];
+      int rw[NB][2], ln[NB][2];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int b = wid + 32 * i;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          fz[i][h] = 1;
+          if (b < nsel) {
+            const int sb = order_s[b];
+            const int j = 32 * h + lane;
+            if (j < width_s[sb]) {
+              const int c = sb * k + j;
+              fz[i][h] = st.c_fin[c];
+              rw[i][h] = st.c_row[c];
+              ln[i][h] = st.c_len[c];
+            }
+          }
         }
-        before += __popc(m);
       }
-      if (lane == 0) stat_sel[b] = st.slot_input[s];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int b = wid + 32 * i;
+        if (b >= nsel) break;
+        const int sb = order_s[b];
+        int r = off_s[b];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool a = !fz[i][h];
+          const unsigned m = __ballot_sync(0xffffffffu, a);
+          if (a) {
+            const int rr = r + __popc(m & ((1u << lane) - 1u));
+            st.row_slot[rr] = sb;
+            st.row_cand[rr] = 32 * h + lane;
+            st.row_phys[rr] = sb * k + rw[i][h];
+            st.row_len[rr] = ln[i][h];
+          }
+          r += __popc(m);
+        }
+        if (lane == 0) stat_sel[b] = input_s[sb];
+      }
+    } else {  // generic path (k > 64 or very large n)
+      for (int b = wid; b < nsel; b += NT3 / 32) {
+        const int sb = order_s[b];
+        int r = off_s[b];
+        for (int j0 = 0; j0 < width_s[sb]; j0 += 32) {
+          const int j = j0 + lane;
+          const int c = sb * k + j;
+          const bool a = j < width_s[sb] && !st.c_fin[c];
+          const unsigned m = __ballot_sync(0xffffffffu, a);
+          if (a) {
+            const int rr = r + __popc(m & ((1u << lane) - 1u));
+            st.row_slot[rr] = sb;
+            st.row_cand[rr] = j;
+            st.row_phys[rr] = sb * k + st.c_row[c];
+            st.row_len[rr] = st.c_len[c];
+          }
+          r += __popc(m);
+        }
+        if (lane == 0) stat_sel[b] = input_s[sb];
+      }
     }
   }
   if (tid < n_live) st.live[tid] = live_s[tid];
@@ -289,11 +322,12 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
     status[VS_ST_ADMIT0] = admit0;
     status[VS_ST_CURSOR] = cursor;
     status[VS_ST_DONE] = (n_live == 0) ? 1 : 0;
-    status[VS_ST_ERROR] = sh[1];
-    status[VS_ST_NFIN] = sh[0];
+    status[VS_ST_ERROR] = bad ? VS_ERR_CONFIG : 0;
+    status[VS_ST_NFIN] = nfin;
     status[VS_ST_NLIVE_AFTER] = n_live_after;
     st.counters[0] = n_live;
     st.counters[1] = cursor;
+    st.counters[2] = N;
     *st.n_copy = 0;
   }
 }
