@@ -1,0 +1,85 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): length-balanced snake
+sharding and the final ragged output gather."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2010_02164_b200.harness import shard
+from paper_2010_02164_b200.parallel import gather_results, pack_results
+
+K, L, N_TOTAL = 4, 8, 23
+
+
+def _expected(g):
+    cnt = 1 + g % 3
+    out = []
+    for c in range(cnt):
+        n = 2 + (g + c) % 5
+        out.append((tuple(int((g * 7 + c * 3 + p) % 50) for p in range(n)), -(g + c / 10.0)))
+    return out
+
+
+def _rank_main(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    gids = shard(N_TOTAL, world, rank)
+    n = len(gids)
+    count = torch.zeros(n, dtype=torch.int32)
+    lens = torch.full((n * K,), 99, dtype=torch.int32)  # garbage beyond count must be ignored
+    scores = torch.full((n * K,), 7.0, dtype=torch.float64)
+    toks = torch.full((n * K * L,), -5, dtype=torch.int32)
+    for li, g in enumerate(gids):
+        ex = _expected(int(g))
+        count[li] = len(ex)
+        for c, (t, sc) in enumerate(ex):
+            o = li * K + c
+            lens[o] = len(t)
+            scores[o] = sc
+            toks[o * L:o * L + len(t)] = torch.tensor(t, dtype=torch.int32)
+    res = gather_results(pack_results(count, lens, scores, toks, K, L), N_TOTAL)
+    if rank == 0:
+        got = [[(c.tokens, c.score) for c in res[g]] for g in range(N_TOTAL)]
+        q.put(got)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_gloo_two_rank_gather_reassembles_global_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == [_expected(g) for g in range(N_TOTAL)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_snake_shard_is_a_balanced_partition(world):
+    n = 1000
+    lens = np.sort(np.random.default_rng(0).geometric(1 / 25, n))[::-1]
+    parts = [shard(n, world, r) for r in range(world)]
+    allidx = np.sort(np.concatenate(parts))
+    assert np.array_equal(allidx, np.arange(n))
+    sums = [lens[p].sum() for p in parts]
+    counts = [len(p) for p in parts]
+    assert max(counts) - min(counts) <= 1
+    assert max(sums) / max(1, min(sums)) < 1.05
+    for p in parts:  # each shard stays length-sorted
+        assert np.all(np.diff(lens[p]) <= 0)
