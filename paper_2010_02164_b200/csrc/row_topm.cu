@@ -23,12 +23,14 @@
 // value.  Rows that cannot be proven fall back to an exact warp radix select
 // over 64-bit keys.  Every decision is a pure function of the row.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace vs {
 namespace {
 
 constexpr int WPC = 4;                 // warps per CTA (independent rows)
 constexpr int CAPW = 416;              // per-warp candidate buffer (keys)
+constexpr int FLUSH_MIN = 16;          // raise θ once this many candidates are buffered
 constexpr unsigned FULL = 0xffffffffu;
 
 template <typename T>
@@ -167,10 +169,11 @@ struct Cand {
   int cnt;         // buffer fill (warp-uniform)
 };
 
-// Out-of-line candidate append (kept out of the hot loop's instruction
-// stream): a per-lane bitmask of elements >= θx, then one ballot round per
+// Candidate append (warp-synchronous, taken only when some lane's vector max
+// reaches θ): a per-lane bitmask of elements >= θx, then one ballot round per
 // pending element (usually one round), keys compacted into the warp buffer.
-__device__ __noinline__ Cand append_slow(Cand c, float x0, float x1, float x2, float x3, float x4,
+template <bool INL>
+__device__ __forceinline__ Cand append_fast(Cand c, float x0, float x1, float x2, float x3, float x4,
                                          float x5, float x6, float x7, int n, int tok0,
                                          uint64_t* __restrict__ buf, uint64_t* __restrict__ sel, int Meff,
                                          int flush_at) {
@@ -211,11 +214,11 @@ struct PartSmem {  // per-warp results exchanged between the W warps of a row
 
 // W warps per row (W in {1,2,4}; 4/W rows per CTA).  Warp `part` of a row
 // streams vectors [part*seg, (part+1)*seg); the row's leader warp combines.
-template <typename T, int U>
-__global__ void __launch_bounds__(WPC * 32, 5) row_lse_topm_warp_kernel(
+template <typename T, int U, int MINB>
+__global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
-    int* __restrict__ fb_count, int normalized, int sms) {
+    int* __restrict__ fb_count, int normalized, int sms, int flush_min) {
   constexpr int VEC = 16 / sizeof(T);
   __shared__ uint64_t sbuf[WPC][CAPW];
   __shared__ uint64_t ssel[WPC][VS_MAX_M];
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(WPC * 32, 5) row_lse_topm_warp_kernel(
   uint64_t* buf = sbuf[wid];
   uint64_t* sel = ssel[wid];
   const int Meff = M < V ? M : V;
-  const int flush_at = max(16, Meff + 8);
+  const int flush_at = max(flush_min, Meff + 8);
   const T* __restrict__ row = logits + (int64_t)(active ? r : 0) * ld;
 
   // m starts at a finite floor (logits must be > -1e30 or -inf) so the hot loop
@@ -263,10 +266,10 @@ __global__ void __launch_bounds__(WPC * 32, 5) row_lse_topm_warp_kernel(
     }
     if (__any_sync(FULL, cm >= c.theta_x)) {
       if (VEC == 8)
-        c = append_slow(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
+        c = append_fast<true>(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
                         x[VEC > 6 ? 6 : 0], x[VEC > 7 ? 7 : 0], n, tok0, buf, sel, Meff, flush_at);
       else
-        c = append_slow(c, x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
+        c = append_fast<true>(c, x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
                         -INFINITY, n, tok0, buf, sel, Meff, flush_at);
     }
   };
@@ -471,8 +474,24 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
   // grid covers the worst case over the W the kernel will pick from the live R
   const int grid = max((rows + WPC - 1) / WPC, V >= 4096 ? min(rows, sms * 8) : 0);
   const T* p = static_cast<const T*>(logits);
-  row_lse_topm_warp_kernel<T, 4><<<grid, WPC * 32, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, top_logp,
-                                                            row_lse, fb, norm, sms);
+  static int variant = -1, flush_min = FLUSH_MIN;  // tuning knobs (VS_K1_VARIANT, VS_K1_FLUSH)
+  if (variant < 0) {
+    const char* e = getenv("VS_K1_VARIANT");
+    variant = e ? atoi(e) : 1;
+    const char* f = getenv("VS_K1_FLUSH");
+    if (f) flush_min = atoi(f);
+  }
+#define VS_K1_LAUNCH(U_, B_)                                                                            \
+  row_lse_topm_warp_kernel<T, U_, B_><<<grid, WPC * 32, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, \
+                                                                 top_logp, row_lse, fb, norm, sms, flush_min)
+  switch (variant) {
+    case 0: VS_K1_LAUNCH(4, 5); break;
+    case 2: VS_K1_LAUNCH(4, 6); break;
+    case 3: VS_K1_LAUNCH(3, 7); break;
+    case 4: VS_K1_LAUNCH(2, 10); break;
+    default: VS_K1_LAUNCH(2, 8); break;
+  }
+#undef VS_K1_LAUNCH
   VS_CUDA_RET();
 }
 
