@@ -214,3 +214,21 @@ class RowsScorer:
 
     def score_next(self, enc, cand):
         return self._rows.pop(0)
+
+
+class RecordedRowsScorer:
+    """Replays rows recorded from a device scorer (logits + kernel lse per
+    (input_id, tokens)): float64(fp32(logit - lse)).  Used for decoders whose
+    logits the CPU cannot recompute bit-exactly."""
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, logits: dict, lse: dict):
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self.logits, self.lse = logits, lse
+
+    def encode(self, tokens, input_id: int = 0):
+        return Encoding(input_id, tuple(int(t) for t in tokens), len(tokens))
+
+    def score_next(self, enc, cand):
+        key = (enc.input_id, tuple(cand.tokens))
+        x = np.asarray(self.logits[key], dtype=np.float32)
+        return (x - np.float32(self.lse[key])).astype(np.float32).astype(np.float64)

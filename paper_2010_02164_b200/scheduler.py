@@ -39,7 +39,7 @@ def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast):
     bs = _as_batched(scorer, corpus)
     eng = SearchEngine(config, _vocab(bs))
     if fast and on_step is None and not (flush and config.flush_interval):
-        if not isinstance(bs, HostScorerAdapter):
+        if not isinstance(bs, HostScorerAdapter) and not getattr(bs, "host_sync", False):
             return eng.run_async(corpus, bs, admit_mode=admit, select_mode=select, trace=trace)
     return eng.run(corpus, bs, admit_mode=admit, select_mode=select, flush_enabled=flush,
                    trace=trace, on_step=on_step)

@@ -150,11 +150,15 @@ class LseRecorder:
     can rebuild the exact rows the search saw: float64(fp32(logit - lse)).
     Synchronous driver only (it reads the row list on the host each step)."""
 
-    def __init__(self, inner):
+    host_sync = True
+
+    def __init__(self, inner, record_logits: bool = False):
         self.inner = inner
         self.vocab = inner.vocab
         self.table = {}
+        self.logit_table = {} if record_logits else None
         self._keys = None
+        self._logits = None
 
     def bind(self, engine) -> None:
         self.inner.bind(engine)
@@ -167,6 +171,9 @@ class LseRecorder:
             raise RuntimeError("LseRecorder needs the synchronous driver")
         out = self.inner.logits(engine, R)
         t, L, k = engine.t, engine.max_len, engine.k
+        if self.logit_table is not None and R:
+            lg, code = out
+            self._logits = lg[:R, : self.vocab.size].float().cpu().numpy()
         if R:
             phys = t["row_phys"][:R].long()
             hist = t["hist"].view(-1, L)[phys].cpu().numpy()
@@ -180,6 +187,8 @@ class LseRecorder:
 
     def after_step(self, engine, R) -> None:
         lse = engine.t["row_lse"][:R].cpu().numpy() if R else []
-        for key, v in zip(self._keys, lse):
+        for i, (key, v) in enumerate(zip(self._keys, lse)):
             self.table[key] = np.float32(v)
+            if self.logit_table is not None:
+                self.logit_table[key] = self._logits[i].copy()
         self.inner.after_step(engine, R)

@@ -255,3 +255,48 @@ def test_rows_copy_kernel():
     ref[:, 4, :3] = ref[:, 1, :3]
     ref[:, 7, :5] = ref[:, 2, :5]
     assert torch.equal(buf, ref)
+
+
+def _toy_decoder_run(policy_runner="run_varstream"):
+    P, N, SearchEngine, _, _, LseRecorder = _pkg()
+    from paper_2010_02164_b200.decoder import TransformerScorer
+
+    vocab = P.Vocabulary(300, 0, 2)
+    cfg = P.DecodeConfig(k=5, n=8, epsilon=1 / 4, delta=2.5, max_candidates=3, max_len=20)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(11, 40, 300, mean_len=6.0, clip=30))
+    dec = TransformerScorer(vocab, d=32, heads=4, layers=2, enc_layers=1, ffn=64, max_src=32, seed=3,
+                            tau=3.0, eos_bias=3.0, record_logits=True)
+    rec = LseRecorder(dec, record_logits=True)
+    ev = []
+    out, rep = getattr(P, policy_runner)(corpus, rec, cfg, trace=True, on_step=ev.append)
+    return P, vocab, cfg, corpus, dec, rec, ev, out, rep
+
+
+def test_decoder_kv_cache_with_k4_reorder_matches_full_recompute():
+    """Incremental decoding through the physical-row K/V cache, reordered by
+    K4 from K2's copy plan, reproduces a cache-free forward of every sampled
+    prefix (fp32, tolerance 2e-4)."""
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _toy_decoder_run()
+    assert dec.copies > 0, "no K4 copies exercised"
+    keys = sorted(rec.logit_table)
+    rng = np.random.default_rng(0)
+    sample = [keys[i] for i in rng.choice(len(keys), size=min(60, len(keys)), replace=False)]
+    # prefer long prefixes (more reorders upstream)
+    sample += sorted(keys, key=lambda kk: -len(kk[1]))[:20]
+    for iid, toks in sample:
+        want = dec.full_forward(corpus[iid], toks).cpu().numpy()
+        got = rec.logit_table[(iid, toks)]
+        assert np.max(np.abs(got - want)) < 2e-4, (iid, toks)
+
+
+def test_decoder_decisions_match_oracle_replay():
+    """Every search decision on decoder logits is bit-exact vs the oracle
+    replaying the recorded rows (logits, kernel lse)."""
+    from oracle.scorers import RecordedRowsScorer
+
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _toy_decoder_run()
+    cpu = RecordedRowsScorer(vocab.size, vocab.sos, vocab.eos, rec.logit_table, rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
