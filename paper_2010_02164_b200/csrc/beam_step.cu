@@ -340,6 +340,272 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Immediate finalisation policy (bb/search.py:148-187 _expand_immediate):
+// the full pool (no M cap) ranked by fp64 SUM; the top-2k scan sends EOS
+// proposals straight to the outputs (quota k - emitted) and the rest fill the
+// next beam (<= k), δ-pruned against max(first emitted, first fill).  K1
+// supplies each parent's top-(2k+2) by (logp desc, token asc): the first 2k+1
+// re-sorted by (sum desc, token asc) give the parent's exact top-2k by sum,
+// and entry 2k+2 (the best excluded element) is a sentinel proving that no
+// excluded element can tie the 2k-th sum through fp64 merging of distinct
+// logps (flags InvariantViolation otherwise; needs |score| ~ 2^29 |dlogp|).
+__global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg, vs_state st, int M_rows) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int b = blockIdx.x;
+  if (b >= st.status[VS_ST_NSEL]) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int k = cfg.k;
+  const int s = st.sel[b];
+  const int L = st.slot_lt[s];
+  const int w = st.slot_width[s];
+  const int row0 = st.sel_off[b];
+  const int base = s * k;
+  const int V = cfg.vocab_size;
+  const int Mi = min(2 * k + 1, V);  // list entries per parent (K1 order, re-sorted by sum)
+  const int Mu = min(2 * k, V);      // entries a parent can contribute to the scan
+  const bool has_sent = V > 2 * k + 1;  // K1 entry 2k+1 = best excluded element
+  const int Pmax = k * Mi;
+
+  double* cs = reinterpret_cast<double*>(smem);       // [k]
+  uint64_t* ch = reinterpret_cast<uint64_t*>(cs + k);  // [k]
+  double* ps = reinterpret_cast<double*>(ch + k);     // [Pmax] sum
+  float* pl = reinterpret_cast<float*>(ps + Pmax);    // [Pmax] logp
+  int* pp = reinterpret_cast<int*>(pl + Pmax);        // [Pmax] parent
+  int* pt = pp + Pmax;                                // [Pmax] token
+  int* cl = pt + Pmax;                                // [k]
+  int* cr = cl + k;                                   // [k]
+  int* scan = cr + k;                                 // [2k] pool index by rank
+  int* firstc = scan + 2 * k;                         // [k]
+  int* claimed = firstc + k;                          // [k]
+  int* freel = claimed + k;                           // [k]
+  int* nrow = freel + k;                              // [2k] child row (fill children)
+  int* csrc = nrow + 2 * k;                           // [2k]
+  int* emo = csrc + 2 * k;                            // [k] drain order -> scan index
+  __shared__ int wsm[NT2 / 32];
+  __shared__ int s_err;
+
+  if (tid < w) {
+    cs[tid] = st.c_score[base + tid];
+    ch[tid] = st.c_hash[base + tid];
+    cl[tid] = st.c_len[base + tid];
+    cr[tid] = st.c_row[base + tid];
+  }
+  if (tid < k) {
+    firstc[tid] = 0x7fffffff;
+    claimed[tid] = 0;
+  }
+  if (tid == 0) s_err = 0;
+  // bb/search.py:155-158: no finalized candidate may sit on an immediate beam
+  if (__syncthreads_or(tid < w && st.c_fin[base + tid] != 0)) {
+    if (tid == 0) st.counters[3] = VS_ERR_INVARIANT;
+    return;
+  }
+  // ---- per parent: its Mi entries, re-sorted by (sum desc, token asc) -----------
+  for (int a = tid; a < w; a += NT2) {
+    const int b0 = a * Mi;
+    const double sc = cs[a];
+    bool sorted = true;
+    for (int m = 0; m < Mi; ++m) {
+      const int64_t ri = (int64_t)(row0 + a) * M_rows + m;
+      const float lp = st.top_logp[ri];
+      pl[b0 + m] = lp;
+      pt[b0 + m] = st.top_tok[ri];
+      pp[b0 + m] = a;
+      ps[b0 + m] = sc + (double)lp;  // bb/search.py:163
+      if (m && (ps[b0 + m - 1] < ps[b0 + m] || (ps[b0 + m - 1] == ps[b0 + m] && pt[b0 + m - 1] > pt[b0 + m])))
+        sorted = false;
+    }
+    if (!sorted)
+      for (int m = 1; m < Mi; ++m) {
+        const double sv = ps[b0 + m];
+        const float lv = pl[b0 + m];
+        const int tv = pt[b0 + m];
+        int q = m - 1;
+        while (q >= 0 && (ps[b0 + q] < sv || (ps[b0 + q] == sv && pt[b0 + q] > tv))) {
+          ps[b0 + q + 1] = ps[b0 + q];
+          pl[b0 + q + 1] = pl[b0 + q];
+          pt[b0 + q + 1] = pt[b0 + q];
+          --q;
+        }
+        ps[b0 + q + 1] = sv;
+        pl[b0 + q + 1] = lv;
+        pt[b0 + q + 1] = tv;
+      }
+    if (has_sent) {  // boundary proof against the best excluded element
+      const int64_t ri = (int64_t)(row0 + a) * M_rows + Mi;
+      const float lsent = st.top_logp[ri];
+      const int tsent = st.top_tok[ri];
+      const double ssent = sc + (double)lsent;
+      const int bT = b0 + Mu - 1;  // the parent's 2k-th entry by sum
+      if (ssent == ps[bT] && (pl[bT] != lsent || tsent < pt[bT])) s_err = 1;
+    }
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) st.counters[3] = VS_ERR_INVARIANT;
+    return;
+  }
+  // ---- top-2k scan of the pool (parents' first Mu entries) ------------------------
+  const Pool pool{ps, pp, pt};
+  const int P = w * Mu;
+  const int kk = min(2 * k, P);
+  for (int e0 = tid; e0 < P; e0 += NT2) {
+    const int a = e0 / Mu, m = e0 - a * Mu;
+    const int e = a * Mi + m;
+    int rank = 0;
+    for (int pa = 0; pa < w && rank < kk; ++pa)
+      for (int q = 0; q < Mu && pool.before(pa * Mi + q, e); ++q) ++rank;
+    if (rank < kk) scan[rank] = e;
+  }
+  __syncthreads();
+  // ---- classify: EOS -> emitted (quota), others -> fill (<= k) ----------------------
+  const int emitted0 = st.slot_emitted[s];
+  const int quota = k - emitted0;
+  const int j = tid;
+  const bool in_scan = j < kk;
+  const int ej = in_scan ? scan[j] : 0;
+  const bool iseos = in_scan && pt[ej] == cfg.eos;
+  int n_eos, n_non;
+  const int erank = block_prefix(iseos, wsm, &n_eos);
+  const int frank = block_prefix(in_scan && !iseos, wsm, &n_non);
+  const bool emit = iseos && erank < quota;
+  const bool fill = in_scan && !iseos && frank < k;
+  const int n_emit = min(n_eos, quota), n_fill = min(n_non, k);
+  // anchor = max(first emitted, first fill) (bb/search.py:178-183)
+  double anchor = -INFINITY;
+  {
+    // find first emitted and first fill (lowest scan index of each class)
+    const unsigned be = __ballot_sync(FULLM, emit), bf = __ballot_sync(FULLM, fill);
+    if (lane == 0) wsm[wid] = (be ? (wid * 32 + __ffs(be) - 1) : 0x7fffffff);
+    __syncthreads();
+    int fe = 0x7fffffff;
+    for (int q = 0; q < NT2 / 32; ++q) fe = min(fe, wsm[q]);
+    __syncthreads();
+    if (lane == 0) wsm[wid] = (bf ? (wid * 32 + __ffs(bf) - 1) : 0x7fffffff);
+    __syncthreads();
+    int ff = 0x7fffffff;
+    for (int q = 0; q < NT2 / 32; ++q) ff = min(ff, wsm[q]);
+    __syncthreads();
+    if (fe != 0x7fffffff) anchor = ps[scan[fe]];
+    if (ff != 0x7fffffff) anchor = fmax(anchor, ps[scan[ff]]);
+  }
+  const double cut = cfg.delta != INFINITY ? anchor - cfg.delta : -INFINITY;
+  const bool kept = fill && ps[ej] >= cut;  // fill is score-descending: a prefix
+  int nkept;
+  const int krank = block_prefix(kept, wsm, &nkept);  // child index among kept
+  // ---- fill children: rows (first child inherits), tokens, finalisation -------------
+  int pi = 0, tk = -1, crow = 0, src = -1, cfin = 0, clen = 0;
+  double csc = 0.0;
+  uint64_t chh = 0;
+  if (kept) {
+    pi = pp[ej];
+    tk = pt[ej];
+    csc = ps[ej];
+    chh = prefix_step(ch[pi], tk);
+    clen = cl[pi] + 1;
+    cfin = clen >= cfg.max_len;  // cannot be EOS here (bb/core.py:174)
+    atomicMin(&firstc[pi], krank);
+  }
+  __syncthreads();
+  bool extra = false;
+  if (kept) {
+    if (firstc[pi] == krank) {
+      crow = cr[pi];
+      claimed[crow] = 1;
+    } else {
+      extra = true;
+      src = cr[pi];
+    }
+  }
+  __syncthreads();
+  {
+    int nfree, nextra;
+    const bool fr = tid < k && !claimed[tid];
+    const int fpos = block_prefix(fr, wsm, &nfree);
+    if (fr) freel[fpos] = tid;
+    const int xpos = block_prefix(extra, wsm, &nextra);
+    if (extra) crow = freel[xpos];
+  }
+  if (kept) {
+    nrow[krank] = crow;
+    csrc[krank] = src;
+  }
+  __syncthreads();
+  const int ML = cfg.max_len;
+  // ---- EOS emissions straight from the parent's row + eos (warp per emission) -------
+  const int input = st.slot_input[s];
+  for (int q = wid; q < kk; q += NT2 / 32) {
+    const int e = scan[q];
+    if (pt[e] != cfg.eos) continue;
+    // emission order = scan order among EOS proposals
+    int er = 0;
+    for (int q2 = 0; q2 < q; ++q2) er += pt[scan[q2]] == cfg.eos;
+    if (er >= quota) continue;
+    const int64_t o = (int64_t)input * k + emitted0 + er;
+    const int32_t* srcp = st.hist + (int64_t)(base + cr[pp[e]]) * ML;
+    for (int p = lane; p < L; p += 32) st.out_tok[o * ML + p] = srcp[p];
+    if (lane == 0) {
+      st.out_tok[o * ML + L] = cfg.eos;
+      st.out_len[o] = L + 1;
+      st.out_score[o] = ps[e];
+    }
+  }
+  __syncthreads();  // parents' rows are read above before free rows are overwritten
+  for (int c = wid; c < nkept; c += NT2 / 32) {  // prefix copies for extra children
+    const int sr = csrc[c];
+    if (sr < 0) continue;
+    const int32_t* srcp = st.hist + (int64_t)(base + sr) * ML;
+    int32_t* dstp = st.hist + (int64_t)(base + nrow[c]) * ML;
+    for (int p = lane; p < L; p += 32) dstp[p] = srcp[p];
+  }
+  __syncthreads();
+  if (kept) st.hist[(int64_t)(base + crow) * ML + L] = tk;
+  __syncthreads();
+  // ---- length-cap drain of the kept fill (all cap-finalised) --------------------------
+  int width = nkept, ne = n_emit;
+  if (!cfg.no_drain && L + 1 >= cfg.max_len && nkept > 0) {
+    const int q2 = k - emitted0 - n_emit;
+    const int nd = min(q2, nkept);
+    for (int c = wid; c < nd; c += NT2 / 32) {
+      const int64_t o = (int64_t)input * k + emitted0 + n_emit + c;
+      const int32_t* srcp = st.hist + (int64_t)(base + nrow[c]) * ML;
+      for (int p = lane; p <= L; p += 32) st.out_tok[o * ML + p] = srcp[p];
+      if (lane == 0) st.out_len[o] = L + 1;
+    }
+    // scores of drained children
+    if (kept && krank < nd) st.out_score[(int64_t)input * k + emitted0 + n_emit + krank] = csc;
+    ne = n_emit + nd;
+    width = 0;
+  }
+  // ---- next beam SoA, KV copy plan, slot state ---------------------------------
+  const bool stays = kept && width > 0;
+  if (stays) {
+    st.c_score[base + krank] = csc;
+    st.c_hash[base + krank] = chh;
+    st.c_len[base + krank] = clen;
+    st.c_row[base + krank] = crow;
+    st.c_fin[base + krank] = (uint8_t)cfin;
+    if (src >= 0 && !cfin) {
+      const int slot = atomicAdd(st.n_copy, 1);
+      st.copy_list[3 * slot + 0] = base + src;
+      st.copy_list[3 * slot + 1] = base + crow;
+      st.copy_list[3 * slot + 2] = L;
+    }
+  }
+  const int nact2 = __syncthreads_count(stays && !cfin);
+  if (tid == 0) {
+    const int emitted = emitted0 + ne;
+    st.slot_width[s] = width;
+    st.slot_active[s] = nact2;
+    st.slot_lt[s] = L + 1;
+    st.slot_emitted[s] = emitted;
+    st.out_count[input] = emitted;
+    const bool finished = width == 0 || emitted >= k || L + 1 >= cfg.max_len;
+    if (finished) st.slot_flags[s] |= 2;
+  }
+}
 }  // namespace
 }  // namespace vs
 
@@ -347,8 +613,25 @@ extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
   if (!cfg || !st || cfg->k < 1 || cfg->k > VS_MAX_K || cfg->max_candidates < 1 ||
       cfg->max_candidates > cfg->k || M_rows < 1)
     return VS_ERR_CONFIG;
-  if (cfg->policy != VS_POLICY_DEFERRED) return VS_ERR_CONFIG;  // immediate: see DESIGN.md
   const int k = cfg->k;
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  if (cfg->policy == VS_POLICY_IMMEDIATE) {
+    const int Mi = min(2 * k + 1, cfg->vocab_size);
+    if (M_rows < min(2 * k + 2, cfg->vocab_size) || 2 * k > vs::NT2) return VS_ERR_CONFIG;
+    const int Pmax = k * Mi;
+    const size_t smem = (size_t)2 * k * 8 + (size_t)Pmax * (8 + 4 + 4 + 4) + (size_t)14 * k * 4 + 64;
+    if (smem > 200 * 1024) return VS_ERR_CONFIG;
+    static size_t configured_i = 0;
+    if (smem > 48 * 1024 && smem > configured_i) {
+      if (cudaFuncSetAttribute(vs::beam_step_immediate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return VS_ERR_CUDA;
+      configured_i = smem;
+    }
+    vs::beam_step_immediate_kernel<<<cfg->n, vs::NT2, smem, strm>>>(*cfg, *st, M_rows);
+    VS_CUDA_RET();
+  }
+  if (cfg->policy != VS_POLICY_DEFERRED) return VS_ERR_CONFIG;
   const int Meff = cfg->max_candidates < cfg->vocab_size ? cfg->max_candidates : cfg->vocab_size;
   if (M_rows < Meff) return VS_ERR_CONFIG;
   const int Pmax = k + k * Meff;
@@ -361,6 +644,6 @@ extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
       return VS_ERR_CUDA;
     configured = smem;
   }
-  vs::beam_step_kernel<<<cfg->n, vs::NT2, smem, static_cast<cudaStream_t>(stream)>>>(*cfg, *st, M_rows);
+  vs::beam_step_kernel<<<cfg->n, vs::NT2, smem, strm>>>(*cfg, *st, M_rows);
   VS_CUDA_RET();
 }

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
   int32_t* stat_adm = stat_live + n;
 
   // ---- one round of independent loads -------------------------------------------
+  const int sticky = first ? 0 : st.counters[3];  // device contract error from beam_step
   int n_live = first ? 0 : st.counters[0];
   int cursor = first ? 0 : st.counters[1];
   const int nsel_prev = first ? 0 : status[VS_ST_NSEL];
@@ -322,12 +323,13 @@ __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state s
     status[VS_ST_ADMIT0] = admit0;
     status[VS_ST_CURSOR] = cursor;
     status[VS_ST_DONE] = (n_live == 0) ? 1 : 0;
-    status[VS_ST_ERROR] = bad ? VS_ERR_CONFIG : 0;
+    status[VS_ST_ERROR] = bad ? VS_ERR_CONFIG : sticky;
     status[VS_ST_NFIN] = nfin;
     status[VS_ST_NLIVE_AFTER] = n_live_after;
     st.counters[0] = n_live;
     st.counters[1] = cursor;
     st.counters[2] = N;
+    st.counters[3] = sticky;
     *st.n_copy = 0;
   }
 }

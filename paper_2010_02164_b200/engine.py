@@ -86,9 +86,6 @@ class SearchEngine:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2010_02164_b200 requires a CUDA device (sm_100a); "
                                "there is no CPU fallback")
-        if config.policy is not FinalizationPolicy.DEFERRED:
-            raise ConfigError("the device engine implements the deferred policy "
-                              "(immediate is listed as next work in DESIGN.md)")
         if config.k > N.VS_MAX_K or config.n > N.VS_MAX_SLOTS or config.max_candidates > N.VS_MAX_M:
             raise ConfigError(f"k<= {N.VS_MAX_K}, n <= {N.VS_MAX_SLOTS}, M <= {N.VS_MAX_M} "
                               "in this build")
@@ -98,7 +95,12 @@ class SearchEngine:
         k, n, L = config.k, config.n, config.max_len
         self.k, self.n, self.max_len = k, n, L
         self.capacity = min(config.capacity, n * k)  # a step can never need more rows
-        self.m_rows = m_rows or min(config.max_candidates, vocab.size)
+        immediate = config.policy is FinalizationPolicy.IMMEDIATE
+        if immediate and 2 * config.k + 2 > N.VS_MAX_M:
+            raise ConfigError(f"immediate policy needs 2k+2 <= {N.VS_MAX_M}")
+        # immediate ranks each parent's top-(2k+1) by sum, + 1 sentinel (bb/search.py:159-166)
+        self.m_rows = m_rows or (min(2 * config.k + 2, vocab.size) if immediate
+                                 else min(config.max_candidates, vocab.size))
         dev = self.device
         i32 = dict(dtype=torch.int32, device=dev)
         z = torch.zeros
@@ -122,7 +124,8 @@ class SearchEngine:
         self.status_host = torch.zeros(N.status_ints(n), dtype=torch.int32, pin_memory=True)
         self.cfg = N.VsConfig(k=k, n=n, max_candidates=config.max_candidates, max_len=L,
                               vocab_size=vocab.size, sos=vocab.sos, eos=vocab.eos,
-                              policy=N.VS_POLICY_DEFERRED, capacity=self.capacity,
+                              policy=N.VS_POLICY_IMMEDIATE if immediate else N.VS_POLICY_DEFERRED,
+                              capacity=self.capacity,
                               refill_threshold=refill_threshold(config), delta=config.delta)
         self.state = N.VsState()
         for f in N.STATE_FIELDS:

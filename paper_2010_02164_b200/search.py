@@ -78,6 +78,8 @@ def expand_beam(beam: Beam, score_rows, config: DecodeConfig, vocab: Vocabulary,
     if not beam.candidates:
         raise InvariantViolation("cannot expand an empty beam")
     nact = beam.active_width()
+    if str(getattr(config.policy, "value", config.policy)) == "immediate" and nact != len(beam.candidates):
+        raise InvariantViolation("immediate policy never keeps finalized candidates on the beam")
     if len(score_rows) != nact:
         raise InvariantViolation(f"expected {nact} score rows, got {len(score_rows)}")
     for row in score_rows:

@@ -83,7 +83,7 @@ def test_row_topm_strided_and_normalized_rows():
     assert float(lse.abs().max()) == 0.0
 
 
-EXPAND = [c for c in load("expand_cases.json") if c["config"]["policy"] == "deferred"]
+EXPAND = load("expand_cases.json")
 
 
 def _ocfg(d):
@@ -92,13 +92,13 @@ def _ocfg(d):
 
 
 def test_device_expand_beam_matches_reference_goldens():
-    """Every deferred golden case of the reference's expand_beam (incl. the
-    row-value pre-truncation gap case) through K1+K2 on the device."""
+    """Every golden case of the reference's expand_beam — deferred (incl. the
+    row-value pre-truncation gap case) and immediate — through K1+K2."""
     P, *_ = _pkg()
     for ci, case in enumerate(EXPAND):
         d = case["config"]
         cfg = P.DecodeConfig(k=d["k"], n=1, delta=fl(d["delta"]), max_candidates=d["max_candidates"],
-                             max_len=d["max_len"], policy="deferred")
+                             max_len=d["max_len"], policy=d["policy"])
         v = case["vocab"]
         vocab = P.Vocabulary(v["size"], v["sos"], v["eos"])
         cands = tuple(P.Candidate(tuple(c["tokens"]), fl(c["score"]), c["finalized"])
@@ -157,7 +157,8 @@ RUNS = {f["name"]: f for f in load("runs.json")}
 
 
 @pytest.mark.parametrize("name", ["c1_varstream_eps0.1667", "c1_varbeam", "c1_varfifo",
-                                  "c1_varstream_flush7", "c1_varstream_cap23", "c1_fixedstream"])
+                                  "c1_varstream_flush7", "c1_varstream_cap23", "c1_fixedstream",
+                                  "c1_varstream_immediate"])
 def test_engine_with_reference_scorer_matches_oracle_events(name):
     """Reference workloads (SeededHashScorer) through the device engine via the
     drop-in adapter: StepEvents, trace and outputs bit-exact vs the oracle
@@ -169,7 +170,8 @@ def test_engine_with_reference_scorer_matches_oracle_events(name):
     d = fx["config"]
     cfg = P.DecodeConfig(k=d["k"], n=d["n"], epsilon=d["epsilon"], delta=fl(d["delta"]),
                          max_candidates=d["max_candidates"], max_len=d["max_len"],
-                         capacity=d["capacity"], flush_interval=d["flush_interval"])
+                         capacity=d["capacity"], flush_interval=d["flush_interval"],
+                         policy=d["policy"])
     corpus = [tuple(x) for x in fx["corpus"]][:120]
     vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
     runner = {"run_varstream": P.run_varstream, "run_varbeam": P.run_varbeam,
@@ -187,11 +189,14 @@ def test_engine_with_reference_scorer_matches_oracle_events(name):
 
 
 HASH_CASES = [
-    # name, V, k, n, M, delta, max_len, eps, N, dtype, scale, power, eos_bias
+    # name, V, k, n, M, delta, max_len, eps, N, dtype, scale, power, eos_bias[, policy]
     ("toy_c1", 1000, 5, 32, 3, 1.5, 48, 1 / 6, 160, "bf16", 8.0, 1, 6.0),
     ("toy_fixed", 1000, 5, 32, 5, math.inf, 48, 1 / 6, 96, "f32", 8.0, 1, 6.0),
     ("parse_c3", 2048, 10, 64, 3, 10.0, 40, 1 / 6, 120, "bf16", 6.0, 2, 5.0),
     ("wide_k", 3000, 24, 8, 6, 2.0, 20, 1 / 4, 24, "f32", 10.0, 4, 9.0),
+    ("wmt_like", 42024, 50, 16, 5, 1.5, 40, 1 / 6, 24, "bf16", 0.5, 0, 7.5),
+    ("immediate", 1000, 5, 16, 5, 1.5, 32, 1 / 6, 96, "bf16", 0.5, 0, 4.0, "immediate"),
+    ("immediate_k16", 2048, 16, 8, 16, 3.0, 24, 1 / 4, 40, "f32", 0.5, 0, 4.0, "immediate"),
 ]
 
 
@@ -200,10 +205,12 @@ def test_device_hash_decode_matches_oracle(case):
     """Whole VarStream decodes with the device scorer: every decision, event and
     fp64 score bit-exact vs the oracle replaying the kernel's lse; the async
     (sync-free) driver reproduces the synchronous one."""
-    name, V, k, n, M, delta, ml, eps, Nin, dt, scale, power, eb = case
+    name, V, k, n, M, delta, ml, eps, Nin, dt, scale, power, eb = case[:13]
+    policy = case[13] if len(case) > 13 else "deferred"
     P, N, SearchEngine, DeviceHashScorer, _, LseRecorder = _pkg()
     vocab = P.Vocabulary(V, 0, 2)
-    cfg = P.DecodeConfig(k=k, n=n, epsilon=eps, delta=delta, max_candidates=M, max_len=ml)
+    cfg = P.DecodeConfig(k=k, n=n, epsilon=eps, delta=delta, max_candidates=M, max_len=ml,
+                         policy=policy)
     corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(99, Nin, V, mean_len=8.0))
     rec = LseRecorder(DeviceHashScorer(vocab, 5, scale=scale, power=power, eos_bias=eb, dtype=dt))
     ev = []
