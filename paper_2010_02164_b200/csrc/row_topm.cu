@@ -28,9 +28,12 @@
 namespace vs {
 namespace {
 
-constexpr int WPC = 4;                 // warps per CTA (independent rows)
+constexpr int WPC = 8;                 // warps per CTA (W warps per row, WPC/W rows)
 constexpr int CAPW = 416;              // per-warp candidate buffer (keys)
-constexpr int FLUSH_MIN = 16;          // raise θ once this many candidates are buffered
+constexpr int FLUSH_MIN = 16;
+#ifndef PICKW_C0
+#define PICKW_C0 0.5f  // per-task fixed cost relative to streaming one row
+#endif          // raise θ once this many candidates are buffered
 constexpr unsigned FULL = 0xffffffffu;
 
 template <typename T>
@@ -69,17 +72,45 @@ __device__ __forceinline__ float prev_repr<__nv_bfloat16>(float x) {
   return __uint_as_float((u & 0x80000000u) ? u + 0x10000u : u - 0x10000u);
 }
 
+// Packed fp32x2 helpers (sm_100: FFMA2 / FADD2 / FMUL2 issue two lanes of work).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(unsigned long long v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b,
+                                                   unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// Bulk L2 prefetch (TMA engine, no registers / smem held while in flight).
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
+  return e;
+}
+
 // logit key: larger = earlier in (value desc, token asc).
 __device__ __forceinline__ uint64_t vkey(float x, int tok) {
   return ((uint64_t)ord_f32(x) << 32) | (uint64_t)(0xffffffffu - (uint32_t)tok);
 }
-
-struct WarpState {
-  float m, s0, s1;    // online log-sum-exp (two partial sums)
-  uint64_t theta;     // candidate threshold key (warp-uniform); 0 = everything passes
-  float theta_x;      // logit part of theta (-inf when theta == 0)
-  int cnt;            // buffer fill (warp-uniform)
-};
 
 // Keep the top-`keep` keys of buf[0..cnt) in buf[0..keep) (sorted desc) using
 // `keep` warp-argmax rounds; returns the keep-th key (0 if fewer entries).
@@ -198,11 +229,33 @@ __device__ __forceinline__ Cand append_fast(Cand c, float x0, float x1, float x2
   }
   if (c.cnt >= flush_at) {
     __syncwarp();
-    c.theta = warp_select(buf, c.cnt, Meff, sel);
-    c.theta_x = unord_f32((uint32_t)(c.theta >> 32));
+    const uint64_t th = warp_select(buf, c.cnt, Meff, sel);
+    if (th > c.theta) {
+      c.theta = th;
+      c.theta_x = unord_f32((uint32_t)(th >> 32));
+    }
     c.cnt = Meff;
   }
   return c;
+}
+
+// Warps per row from the live row count: minimise the makespan
+// ceil(R*W/T) * (c0 + 1/W) over W in {1,2,4,8} (T = resident warps, c0 =
+// per-task boot/epilogue cost relative to streaming a whole row) — balances
+// wave quantisation against the per-warp fixed cost.
+__host__ __device__ __forceinline__ int pick_w(int R, int V, int T) {
+  if (V < 4096 || R <= 0) return 1;
+  int best = 1;
+  float bc = 1e30f;
+  for (int w = 1; w <= WPC; w <<= 1) {
+    const float waves = (float)(((long)R * w + T - 1) / T);
+    const float cost = waves * (PICKW_C0 + 1.0f / w);
+    if (cost < bc - 1e-6f) {
+      bc = cost;
+      best = w;
+    }
+  }
+  return best;
 }
 
 struct PartSmem {  // per-warp results exchanged between the W warps of a row
@@ -218,7 +271,8 @@ template <typename T, int U, int MINB>
 __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
-    int* __restrict__ fb_count, int normalized, int sms, int flush_min) {
+    int* __restrict__ fb_count, int normalized, int sms, int flush_min, int pf_batches,
+    int warps_per_sm) {
   constexpr int VEC = 16 / sizeof(T);
   __shared__ uint64_t sbuf[WPC][CAPW];
   __shared__ uint64_t ssel[WPC][VS_MAX_M];
@@ -226,9 +280,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   __shared__ PartSmem spart[WPC];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = d_R ? *d_R : R_host;
-  // warps per row from the live row count: enough warps for small steps, one
-  // warp per row once rows alone fill the machine
-  const int W = (V < 4096) ? 1 : (R < sms * 8 ? 4 : (R < sms * 16 ? 2 : 1));
+  const int W = pick_w(R, V, sms * warps_per_sm);
   const int part = wid % W, leader = wid - part;
   const int r = blockIdx.x * (WPC / W) + wid / W;
   if (blockIdx.x * (WPC / W) >= R) return;  // whole CTA idle (uniform)
@@ -243,7 +295,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   // needs no -inf guards: ex2(x*log2e - m*log2e) is 0 for x = -inf and the
   // branchless rescale ex2((m_old - m_new)*log2e) is 0 on the first vector.
   constexpr float M_FLOOR = -1e30f;
-  float m = M_FLOOR, s0 = 0.0f, s1 = 0.0f;
+  float m = M_FLOOR;
+  unsigned long long s01 = pk2(0.0f, 0.0f);  // (even, odd) partial sums of exp(x - m)
+  const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
   Cand c{0ull, -INFINITY, 0};
 
   auto consume = [&](const float (&x)[VEC], int n, int tok0) {
@@ -251,18 +305,16 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
 #pragma unroll
     for (int j = 1; j < VEC; ++j) cm = fmaxf(cm, x[j]);
     const float mn = fmaxf(m, cm);
-    float sc;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(sc) : "f"((m - mn) * VS_LOG2E));
-    s0 *= sc;
-    s1 *= sc;
+    const float sc = ex2f((m - mn) * VS_LOG2E);  // branchless online rescale
+    s01 = mul2(s01, pk2(sc, sc));
     m = mn;
-    const float ml = m * VS_LOG2E;
+    const float nml = -m * VS_LOG2E;
+    const unsigned long long nml2 = pk2(nml, nml);
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) {
-      float e;
-      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fmaf(x[j], VS_LOG2E, -ml)));
-      if (j & 1) s1 += e;
-      else s0 += e;
+    for (int j = 0; j < VEC; j += 2) {
+      float t0, t1;
+      up2(fma2(pk2(x[j], x[j + 1]), L2E2, nml2), t0, t1);  // FFMA2: x*log2e - m*log2e
+      s01 = add2(s01, pk2(ex2f(t0), ex2f(t1)));          // FADD2
     }
     if (__any_sync(FULL, cm >= c.theta_x)) {
       if (VEC == 8)
@@ -322,8 +374,17 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
       }
     }
     int base = v0;
+    const int pf_dist = 2 * BATCH * pf_batches;  // vectors ahead of the demand loads
+    if (lane == 0 && pf_batches > 0) {  // prime the L2 prefetch window
+      const int p1 = min(v1, v0 + pf_dist);
+      if (p1 > v0 + 2 * BATCH) l2_prefetch(vrow + v0 + 2 * BATCH, (unsigned)(p1 - v0 - 2 * BATCH) * 16u);
+    }
     // full double-batches: no per-vector bounds checks
     for (; base + 2 * BATCH <= v1; base += 2 * BATCH) {
+      if (lane == 0 && pf_batches > 0) {
+        const int p0 = base + pf_dist, p1 = min(v1, p0 + 2 * BATCH);
+        if (p1 > p0) l2_prefetch(vrow + p0, (unsigned)(p1 - p0) * 16u);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         float x[VEC];
@@ -374,7 +435,12 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     }
   }
   // ---- per-warp lse partial -> exchange --------------------------------------------
-  float s = s0 + s1;
+  float s;
+  {
+    float a, b;
+    up2(s01, a, b);
+    s = a + b;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float m2 = __shfl_xor_sync(FULL, m, o);
@@ -471,25 +537,41 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // grid covers the worst case over the W the kernel will pick from the live R
-  const int grid = max((rows + WPC - 1) / WPC, V >= 4096 ? min(rows, sms * 8) : 0);
-  const T* p = static_cast<const T*>(logits);
-  static int variant = -1, flush_min = FLUSH_MIN;  // tuning knobs (VS_K1_VARIANT, VS_K1_FLUSH)
+  static int variant = -1, flush_min = FLUSH_MIN, pf = 0;  // knobs: VS_K1_VARIANT/_FLUSH/_PF
   if (variant < 0) {
+    const char* q = getenv("VS_K1_PF");
+    if (q) pf = atoi(q);
     const char* e = getenv("VS_K1_VARIANT");
-    variant = e ? atoi(e) : 1;
+    variant = e ? atoi(e) : 3;
     const char* f = getenv("VS_K1_FLUSH");
     if (f) flush_min = atoi(f);
   }
+  const int ctas_per_sm = variant == 0 ? 2 : (variant == 3 ? 3 : 4);
+  const int Tw = sms * ctas_per_sm * WPC;
+  // grid covers the worst case over the W the kernel will pick from the live R
+  int grid;
+  if (d_R) {
+    static int cached_rows = -1, cached_grid = 0, cached_T = 0;
+    if (rows != cached_rows || Tw != cached_T) {
+      int g = 1;
+      for (int r = 1; r <= rows; ++r) g = max(g, (r * pick_w(r, V, Tw) + WPC - 1) / WPC);
+      cached_rows = rows;
+      cached_T = Tw;
+      cached_grid = g;
+    }
+    grid = cached_grid;
+  } else {
+    grid = (rows * pick_w(rows, V, Tw) + WPC - 1) / WPC;
+  }
+  const T* p = static_cast<const T*>(logits);
 #define VS_K1_LAUNCH(U_, B_)                                                                            \
   row_lse_topm_warp_kernel<T, U_, B_><<<grid, WPC * 32, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, \
-                                                                 top_logp, row_lse, fb, norm, sms, flush_min)
+                                                                 top_logp, row_lse, fb, norm, sms, flush_min, pf, \
+                                                                 ctas_per_sm * WPC)
   switch (variant) {
-    case 0: VS_K1_LAUNCH(4, 5); break;
-    case 2: VS_K1_LAUNCH(4, 6); break;
-    case 3: VS_K1_LAUNCH(3, 7); break;
-    case 4: VS_K1_LAUNCH(2, 10); break;
-    default: VS_K1_LAUNCH(2, 8); break;
+    case 0: VS_K1_LAUNCH(4, 2); break;
+    case 3: VS_K1_LAUNCH(3, 3); break;
+    default: VS_K1_LAUNCH(2, 4); break;
   }
 #undef VS_K1_LAUNCH
   VS_CUDA_RET();

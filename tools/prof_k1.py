@@ -1,28 +1,55 @@
-"""Standalone K1 driver for ncu: full-width WMT step (R=6400 x |V|=42024 bf16)."""
+"""Standalone K1 timing / ncu driver: R rows x |V| logits (log-like values).
+
+    python tools/prof_k1.py [R] [V] [M] [f32|bf16] [--noflush]
+
+Outputs are pre-allocated and K1 is launched through the C-ABI directly, so
+the CUDA events bracket only the kernel (an L2-flush kernel runs before each
+timed launch unless --noflush).
+"""
 import sys
 from pathlib import Path
 
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_2010_02164_b200.search import row_lse_topm  # noqa: E402
+from paper_2010_02164_b200 import _native as N  # noqa: E402
 
-R = int(sys.argv[1]) if len(sys.argv) > 1 else 6400
-V = int(sys.argv[2]) if len(sys.argv) > 2 else 42024
-M = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-dt = torch.float32 if (len(sys.argv) > 4 and sys.argv[4] == "f32") else torch.bfloat16
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+R = int(args[0]) if len(args) > 0 else 6400
+V = int(args[1]) if len(args) > 1 else 42024
+M = int(args[2]) if len(args) > 2 else 5
+f32 = len(args) > 3 and args[3] == "f32"
+flush_between = "--noflush" not in sys.argv
+dt = torch.float32 if f32 else torch.bfloat16
 g = torch.Generator(device="cuda").manual_seed(0)
 u = torch.rand((R, V), device="cuda", generator=g).clamp_min_(2.0 ** -24)
 x = (-0.5 * torch.log2(u)).to(dt)
 del u
+tok = torch.empty((R, M), dtype=torch.int32, device="cuda")
+lp = torch.empty((R, M), dtype=torch.float32, device="cuda")
+lse = torch.empty((R,), dtype=torch.float32, device="cuda")
+fb = torch.zeros((1,), dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+lib = N.load_library()
+code = N.VS_DTYPE_F32 if f32 else N.VS_DTYPE_BF16
+stream = torch.cuda.current_stream().cuda_stream
+
+
+def launch():
+    N.check(lib.vs_row_lse_topm(x.data_ptr(), code, x.stride(0), V, M, R, None, R, tok.data_ptr(),
+                                lp.data_ptr(), lse.data_ptr(), fb.data_ptr(), stream), "k1")
+
+
 ts = []
-for i in range(6):
-    flush.fill_(i)
+for i in range(8):
+    if flush_between:
+        flush.fill_(i)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    row_lse_topm(x, M)
+    launch()
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print("K1 ms per launch:", [round(t, 4) for t in ts], "GB/s:", round(R * V * x.element_size() / min(ts[2:]) / 1e6, 1))
+best = min(ts[2:])
+print("K1 ms per launch:", [round(t, 4) for t in ts], "GB/s:",
+      round(R * V * x.element_size() / best / 1e6, 1), "fallbacks:", int(fb.item()))
