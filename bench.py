@@ -180,6 +180,55 @@ def full_width_k1(w, iters: int = 20):
     return R * w["V"] * 2, t, int(fb.item())
 
 
+def engines_comparison(reps: int = 3):
+    """BASELINE.json configs[1]: Fixed vs VarBeam vs VarStream (ε sweep) on the
+    toy workload, same device scorer; decoded seq/s (device-resident inputs),
+    timesteps and expansions/step per engine.  Outputs are identical across
+    var-width engines (tested); only scheduling differs."""
+    import math
+
+    import torch
+
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary
+    from paper_2010_02164_b200 import _native as N
+    from paper_2010_02164_b200.engine import SearchEngine
+    from paper_2010_02164_b200.harness import flatten
+    from paper_2010_02164_b200.scorers import DeviceHashScorer
+
+    w = WORKLOADS["toy_c1"]
+    corpus = _corpus(w)
+    vocab = Vocabulary(w["V"], w["sos"], w["eos"])
+    tok, off = flatten(corpus)
+    d_tok, d_off = torch.from_numpy(tok).cuda(), torch.from_numpy(off).cuda()
+    out = {}
+    runs = [("fixed", N.VS_ADMIT_VARBEAM, 1 / 6, math.inf, w["k"]),
+            ("varbeam", N.VS_ADMIT_VARBEAM, 1 / 6, w["delta"], w["M"]),
+            ("fixedstream", N.VS_ADMIT_VARSTREAM, 1 / 6, math.inf, w["k"])]
+    runs += [(f"varstream_eps1/{d}", N.VS_ADMIT_VARSTREAM, 1 / d, w["delta"], w["M"]) for d in (8, 6, 4)]
+    for name, admit, eps, delta, M in runs:
+        cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=eps, delta=delta, max_candidates=M,
+                           max_len=w["max_len"])
+        eng = SearchEngine(cfg, vocab)
+        sc = DeviceHashScorer(vocab, w["scorer_seed"], scale=w["scale"], power=w["power"],
+                              eos_bias=w["eos_bias"], dtype=w["dtype"])
+        ts = []
+        for i in range(reps + 1):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, rep = eng.run_async(None, sc, admit_mode=admit, select_mode=N.VS_SELECT_MIN_LT,
+                                   src_tok=d_tok, src_off=d_off, materialize=False)
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        t = statistics.median(ts)
+        out[name] = {"seq_per_s": round(len(corpus) / t, 1), "timesteps": rep.timesteps,
+                     "expansions": rep.candidate_expansions,
+                     "expansions_per_step": round(rep.expansions_per_step, 1)}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -319,6 +368,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if rank == 0 and world == 1:
+        line["engines_toy_c2"] = engines_comparison()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",

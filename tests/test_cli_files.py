@@ -1,0 +1,78 @@
+"""CLI and file formats (drop-in for bb/cli.py and bb/harness.py I/O)."""
+import json
+
+import pytest
+
+from paper_2010_02164_b200 import cli
+from paper_2010_02164_b200.harness import (ResultsDocument, generate_synthetic_corpus, load_corpus,
+                                           save_corpus)
+from paper_2010_02164_b200.errors import DataError
+
+
+def test_corpus_round_trip_and_errors(tmp_path):
+    c = [(1, 2, 3), (4,), (5, 6)]
+    p = tmp_path / "c.txt"
+    save_corpus(c, p)
+    assert load_corpus(p) == c
+    (tmp_path / "bad.txt").write_text("1 2\nx 3\n")
+    with pytest.raises(DataError, match="line 2"):
+        load_corpus(tmp_path / "bad.txt")
+    (tmp_path / "neg.txt").write_text("1 -2\n")
+    with pytest.raises(DataError, match="negative"):
+        load_corpus(tmp_path / "neg.txt")
+    (tmp_path / "empty.txt").write_text("\n\n")
+    with pytest.raises(DataError, match="empty"):
+        load_corpus(tmp_path / "empty.txt")
+
+
+def test_results_document_round_trip(tmp_path):
+    doc = ResultsDocument("varstream", {"decode": {"k": 2}}, {"timesteps": 3},
+                          [{"input_id": 0, "candidates": [{"tokens": [0, 5, 1], "score": -1.25}]}])
+    doc.write(tmp_path / "r.json")
+    back = ResultsDocument.read(tmp_path / "r.json")
+    assert back.to_dict() == doc.to_dict()
+
+
+def test_generator_matches_reference_golden_corpus():
+    from goldens import load
+
+    fx = load("runs.json")[0]  # generate_synthetic_corpus(4242, 240, 50, mean 8) by the reference
+    got = generate_synthetic_corpus(4242, 240, 50, mean_len=8.0)
+    assert [list(x) for x in got] == fx["corpus"]
+
+
+@pytest.mark.parametrize("argv,code", [
+    (["--engine", "varstream"], 1),                                      # k/n missing
+    (["--engine", "bogus", "--k", "2", "--n", "2"], 1),                 # bad flag value
+    (["--engine", "varstream", "--k", "2", "--n", "2"], 1),             # model missing
+    (["--engine", "varstream", "--k", "2", "--n", "2", "--delta", "x"], 1),
+])
+def test_cli_config_errors_exit_1(argv, code, capsys):
+    assert cli.main(argv) == code
+
+
+def test_cli_missing_model_file_exits_2(tmp_path):
+    assert cli.main(["--engine", "varstream", "--k", "2", "--n", "2", "--model",
+                     str(tmp_path / "nope.json"), "--corpus", str(tmp_path / "c.txt")]) == 2
+
+
+def test_cli_unknown_model_kind_exits_2(tmp_path):
+    m = tmp_path / "m.json"
+    m.write_text(json.dumps({"kind": "mystery", "vocab_size": 10, "sos": 0, "eos": 1}))
+    assert cli.main(["--engine", "varstream", "--k", "2", "--n", "2", "--model", str(m),
+                     "--corpus", str(tmp_path / "c.txt")]) == 2
+
+
+@pytest.mark.gpu
+def test_cli_device_run_writes_results_and_trace(tmp_path):
+    m = tmp_path / "m.json"
+    m.write_text(json.dumps({"kind": "device_hash", "vocab_size": 1000, "sos": 0, "eos": 2, "seed": 3,
+                             "eos_bias": 4.0}))
+    out = tmp_path / "r.json"
+    cfgf = tmp_path / "cfg.json"
+    cfgf.write_text(json.dumps({"engine": "varstream", "corpus": {"synthetic": {"n_inputs": 40, "mean_len": 6}},
+                                "decode": {"k": 5, "n": 8, "delta": "1.5", "max_candidates": 3, "max_len": 30}}))
+    assert cli.main(["--config", str(cfgf), "--model", str(m), "--out", str(out), "--trace"]) == 0
+    doc = ResultsDocument.read(out)
+    assert len(doc.records) == 40 and all(1 <= len(r["candidates"]) <= 5 for r in doc.records)
+    assert (tmp_path / "r.json.trace.csv").read_text().startswith("timestep,expansions")
