@@ -28,6 +28,7 @@
 #ifndef VARSTREAM_H_
 #define VARSTREAM_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -44,6 +45,10 @@ extern "C" {
 /* OR-ed into dtype: rows are already log-probs (reference Scorer rows,
  * bb/model.py:86); lse is taken as 0 so logp = fp32(row). */
 #define VS_ROWS_NORMALIZED 0x100
+/* OR-ed into dtype for vs_row_lse_topm_ws: pin the K1 kernel (default: the
+ * split-row TMA kernel for 8 < M <= 32, the warp-per-row kernel otherwise). */
+#define VS_K1_SPLIT 0x200
+#define VS_K1_WARP 0x400
 
 #define VS_POLICY_DEFERRED 0  /* bb/core.py:18-28 FinalizationPolicy */
 #define VS_POLICY_IMMEDIATE 1
@@ -161,6 +166,22 @@ int vs_version(void);
 int vs_row_lse_topm(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
                     int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,
                     float* top_logp, float* row_lse, int32_t* fallback_count, void* stream);
+
+/* K1 with a caller-provided workspace — same contract and outputs as
+ * vs_row_lse_topm.  When the rows qualify (16-byte aligned logits and
+ * ld*sizeof(T), 4 KB <= V*sizeof(T) <= 256 KB, M <= 32) it runs the
+ * TMA-staged split-row kernel (csrc/row_topm_tma.cu): a persistent grid whose
+ * warps stream equal slices of the R x |V| logits through cp.async.bulk
+ * shared-memory rings, so small steps still fill all 148 SMs.  Its lse is a
+ * partition-invariant function of the row (independent of R).  Otherwise it
+ * behaves exactly like vs_row_lse_topm.  The workspace must hold
+ * vs_row_lse_topm_ws_bytes(R_grid, V, dtype) bytes and be ZEROED ONCE when
+ * allocated (per-row counters return to zero after every launch). */
+int vs_row_lse_topm_ws(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
+                       int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,
+                       float* top_logp, float* row_lse, int32_t* fallback_count, void* workspace,
+                       size_t workspace_bytes, void* stream);
+size_t vs_row_lse_topm_ws_bytes(int32_t R_grid, int32_t V, int32_t dtype);
 
 /* K2  beam_step — replaces bb/search.py:76-145 (expand_beam, deferred),
  * :148-187 (immediate), :190-230 (length-cap drain, advance_beam) and

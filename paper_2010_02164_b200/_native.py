@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvarstream.so"
 
 VS_OK, VS_ERR_CONFIG, VS_ERR_INVARIANT, VS_ERR_CUDA = 0, -1, -3, -4
 VS_DTYPE_F32, VS_DTYPE_BF16, VS_ROWS_NORMALIZED = 0, 1, 0x100
+VS_K1_SPLIT, VS_K1_WARP = 0x200, 0x400  # pin the K1 kernel (vs_row_lse_topm_ws)
 VS_POLICY_DEFERRED, VS_POLICY_IMMEDIATE = 0, 1
 VS_ADMIT_NONE, VS_ADMIT_VARSTREAM, VS_ADMIT_VARBEAM, VS_ADMIT_VARFIFO = -1, 0, 1, 2
 VS_SELECT_MIN_LT, VS_SELECT_FIFO, VS_SELECT_ALL = 0, 1, 2
@@ -58,7 +59,7 @@ class VsHashParams(C.Structure):
 
 
 # Every symbol include/varstream.h declares (checked by tests/test_native_exports.py).
-EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_beam_step", "vs_schedule", "vs_rows_copy",
+EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step", "vs_schedule", "vs_rows_copy",
            "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits")
 
 _lib = None
@@ -77,6 +78,9 @@ def load_library(path: Path | None = None) -> C.CDLL:
     sig = {
         "vs_version": ([], i32),
         "vs_row_lse_topm": ([vp, i32, i64, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp], i32),
+        "vs_row_lse_topm_ws": ([vp, i32, i64, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, C.c_size_t, vp],
+                               i32),
+        "vs_row_lse_topm_ws_bytes": ([i32, i32, i32], C.c_size_t),
         "vs_beam_step": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, vp], i32),
         "vs_schedule": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp], i32),
         "vs_rows_copy": ([vp, i64, i32, i64, i64, vp, vp, i32, vp], i32),

@@ -578,9 +578,41 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
 }
 
 }  // namespace
+
+// row_topm_tma.cu
+bool tma_eligible(const void* logits, int64_t ld, int V, int M, int esize, bool pinned);
+template <typename T>
+int launch_tma(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int R_grid,
+               int* top_tok, float* top_logp, float* row_lse, int* fb, int norm, void* ws, size_t ws_bytes,
+               cudaStream_t st);
 }  // namespace vs
 
-extern "C" int vs_version(void) { return 2; }
+extern "C" int vs_version(void) { return 3; }
+
+extern "C" int vs_row_lse_topm_ws(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
+                                  int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,
+                                  float* top_logp, float* row_lse, int32_t* fallback_count, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (!logits || !top_tok || !top_logp || V < 1 || M < 1 || M > VS_MAX_M || ld < V || R_grid < 0)
+    return VS_ERR_CONFIG;
+  if (R_grid == 0) return VS_OK;
+  const int norm = (dtype & VS_ROWS_NORMALIZED) ? 1 : 0;
+  const int pin = dtype & (VS_K1_SPLIT | VS_K1_WARP);
+  const int dt = dtype & ~(VS_ROWS_NORMALIZED | VS_K1_SPLIT | VS_K1_WARP);
+  dtype &= ~(VS_K1_SPLIT | VS_K1_WARP);
+  const int es = dt == VS_DTYPE_F32 ? 4 : 2;
+  if (workspace && (dt == VS_DTYPE_F32 || dt == VS_DTYPE_BF16) && !(pin & VS_K1_WARP) &&
+      vs::tma_eligible(logits, ld, V, M, es, (pin & VS_K1_SPLIT) != 0)) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dt == VS_DTYPE_F32)
+      return vs::launch_tma<float>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse,
+                                   fallback_count, norm, workspace, workspace_bytes, st);
+    return vs::launch_tma<__nv_bfloat16>(logits, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse,
+                                         fallback_count, norm, workspace, workspace_bytes, st);
+  }
+  return vs_row_lse_topm(logits, dtype, ld, V, M, R_host, d_R, R_grid, top_tok, top_logp, row_lse,
+                         fallback_count, stream);
+}
 
 extern "C" int vs_row_lse_topm(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
                                int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,

@@ -132,6 +132,7 @@ class SearchEngine:
             if f in self.t:
                 setattr(self.state, f, self.t[f].data_ptr())
         self.N = 0
+        self._k1_ws = None
 
     # ------------------------------------------------------------------ data
     @property
@@ -198,10 +199,15 @@ class SearchEngine:
     def row_topm(self, logits: torch.Tensor, dtype_code: int, R_host: int, R_grid: int,
                  d_R: int | None = None) -> None:
         ld = logits.stride(0)
-        N.check(self.lib.vs_row_lse_topm(
+        nbytes = int(self.lib.vs_row_lse_topm_ws_bytes(self.capacity, self.vocab.size, dtype_code))
+        ws = self._k1_ws
+        if ws is None or ws.numel() < nbytes:  # zeroed once; counters self-reset
+            ws = self._k1_ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        N.check(self.lib.vs_row_lse_topm_ws(
             logits.data_ptr(), dtype_code, ld, self.vocab.size, self.m_rows, R_host, d_R, R_grid,
             self.t["top_tok"].data_ptr(), self.t["top_logp"].data_ptr(), self.t["row_lse"].data_ptr(),
-            self.t["fallbacks"].data_ptr(), self.stream_ptr), "vs_row_lse_topm")
+            self.t["fallbacks"].data_ptr(), ws.data_ptr(), ws.numel(), self.stream_ptr),
+            "vs_row_lse_topm_ws")
 
     def beam_step(self) -> None:
         N.check(self.lib.vs_beam_step(C.byref(self.cfg), C.byref(self.state), self.m_rows,

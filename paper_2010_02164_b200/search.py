@@ -19,24 +19,53 @@ from .engine import SearchEngine
 from .errors import InvariantViolation
 
 
-def row_lse_topm(logits: torch.Tensor, M: int, *, normalized: bool = False):
+_WS: dict = {}
+
+
+def k1_workspace(R_grid: int, V: int, code: int, device) -> torch.Tensor:
+    """Zeroed K1 workspace (per-row counters return to zero after every
+    launch, so one allocation serves every later call with the same V and
+    dtype on the device; its layout depends on V and dtype only)."""
+    lib = N.load_library()
+    nbytes = int(lib.vs_row_lse_topm_ws_bytes(R_grid, V, code))
+    key = (str(device), V, code & ~N.VS_ROWS_NORMALIZED)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def row_lse_topm(logits: torch.Tensor, M: int, *, normalized: bool = False, legacy: bool = False,
+                 kernel: str = "auto"):
     """K1 over a [R, V] device tensor (fp32 or bf16; rows may be strided).
-    Returns (tokens int32 [R, M], logp fp32 [R, M], lse fp32 [R], fallbacks)."""
+    Returns (tokens int32 [R, M], logp fp32 [R, M], lse fp32 [R], fallbacks).
+    `kernel`: "auto" (library dispatch), "split" (TMA split-row kernel when
+    the rows qualify) or "warp" (warp-per-row kernel); `legacy` calls the
+    workspace-free entry point (always the warp-per-row kernel)."""
     if logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a row-major [R, V] tensor")
     R, V = logits.shape
     code = {torch.float32: N.VS_DTYPE_F32, torch.bfloat16: N.VS_DTYPE_BF16}[logits.dtype]
     if normalized:
         code |= N.VS_ROWS_NORMALIZED
+    pin = {"auto": 0, "split": N.VS_K1_SPLIT, "warp": N.VS_K1_WARP}[kernel]
     dev = logits.device
     tok = torch.empty((R, M), dtype=torch.int32, device=dev)
     lp = torch.empty((R, M), dtype=torch.float32, device=dev)
     lse = torch.empty((R,), dtype=torch.float32, device=dev)
     fb = torch.zeros((1,), dtype=torch.int32, device=dev)
     lib = N.load_library()
-    N.check(lib.vs_row_lse_topm(logits.data_ptr(), code, logits.stride(0), V, M, R, None, R,
-                                tok.data_ptr(), lp.data_ptr(), lse.data_ptr(), fb.data_ptr(),
-                                torch.cuda.current_stream(dev).cuda_stream), "vs_row_lse_topm")
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if legacy:
+        N.check(lib.vs_row_lse_topm(logits.data_ptr(), code, logits.stride(0), V, M, R, None, R,
+                                    tok.data_ptr(), lp.data_ptr(), lse.data_ptr(), fb.data_ptr(),
+                                    stream), "vs_row_lse_topm")
+    else:
+        ws = k1_workspace(R, V, code, dev)
+        N.check(lib.vs_row_lse_topm_ws(logits.data_ptr(), code | pin, logits.stride(0), V, M, R, None, R,
+                                       tok.data_ptr(), lp.data_ptr(), lse.data_ptr(), fb.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), stream), "vs_row_lse_topm_ws")
     return tok, lp, lse, fb
 
 

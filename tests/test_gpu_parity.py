@@ -49,9 +49,10 @@ CASES = [(1000, 3), (1000, 5), (2048, 10), (42024, 5), (42024, 50), (17, 3), (3,
          (33, 16), (1001, 64)]
 
 
+@pytest.mark.parametrize("kernel", ["split", "warp"])
 @pytest.mark.parametrize("V,M", CASES)
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_row_topm_matches_oracle(V, M, dtype):
+def test_row_topm_matches_oracle(V, M, dtype, kernel):
     P, *_ = _pkg()
     rng = np.random.default_rng(V * 131 + M)
     R = 24
@@ -67,7 +68,75 @@ def test_row_topm_matches_oracle(V, M, dtype):
     if dtype == "bf16":
         t = t.to(torch.bfloat16)
         x = t.float().cpu().numpy()
-    tok, lp, lse, fb = P.row_lse_topm(t, M)
+    tok, lp, lse, fb = P.row_lse_topm(t, M, kernel=kernel)
+    torch.cuda.synchronize()
+    _check_rows(x, M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
+
+
+def _rows(rng, R, V, kind):
+    if kind == "normal":
+        return rng.normal(0, 3, (R, V)).astype(np.float32)
+    u = rng.random((R, V)).clip(2.0 ** -24)                 # log-like (the decode's scorer)
+    return (-0.5 * np.log2(u)).astype(np.float32)
+
+
+@pytest.mark.parametrize("M", [5, 32])
+@pytest.mark.parametrize("R", [1, 3, 37, 600, 2000])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_row_topm_tma_split_rows(R, dtype, M):
+    """The TMA split-row kernel at step sizes from 1 row (a row spread over
+    many warps) to 2000 rows (whole rows per warp), checked row by row on a
+    sample against the oracle (given the kernel's lse)."""
+    P, *_ = _pkg()
+    rng = np.random.default_rng(R)
+    V = 42024
+    x = _rows(rng, R, V, "loglike" if R % 2 else "normal")
+    t = torch.from_numpy(x).cuda()
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16)
+        x = t.float().cpu().numpy()
+    tok, lp, lse, fb = P.row_lse_topm(t, M, kernel="split")
+    torch.cuda.synchronize()
+    pick = sorted(set(np.linspace(0, R - 1, min(R, 24)).astype(int).tolist()))
+    _check_rows(x[pick], M, tok.cpu().numpy()[pick], lp.cpu().numpy()[pick], lse.cpu().numpy()[pick])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_row_topm_tma_lse_is_partition_invariant(dtype):
+    """lse (hence every logp) of a row is a function of the row alone: the same
+    row scored alone, among 5 rows, or among 900 rows (different split of its
+    segments over warps) gives bit-identical outputs."""
+    P, *_ = _pkg()
+    rng = np.random.default_rng(11)
+    V, M = 42024, 8
+    base = rng.normal(0, 2, (900, V)).astype(np.float32)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    big = torch.from_numpy(base).cuda().to(tdt)
+    outs = []
+    for lo, hi in [(450, 451), (448, 453), (0, 900), (300, 901)]:
+        tok, lp, lse, _ = P.row_lse_topm(big[lo:hi].contiguous(), M, kernel="split")
+        outs.append((tok[450 - lo].cpu(), lp[450 - lo].cpu(), lse[450 - lo].cpu()))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) and torch.equal(o[2], outs[0][2])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_row_topm_tma_scalar_tail_and_ties(dtype):
+    """Rows whose byte length is not a multiple of 16 (scalar tail on the TMA
+    path), ties straddling segment boundaries, and a winner in the tail."""
+    P, *_ = _pkg()
+    rng = np.random.default_rng(5)
+    V, M = 42027, 6
+    big = torch.from_numpy(rng.normal(0, 1, (40, 42032)).astype(np.float32)).cuda()
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    big = big.to(tdt)
+    view = big[:, :V]
+    view[1, V - 1] = 30.0          # winner in the scalar tail
+    view[2, 2047:2049] = 9.0       # tie across the first segment boundary (bf16: 2048 elems/seg)
+    view[2, 1023:1025] = 9.0       # (f32: 1024 elems/seg)
+    view[3, :] = 0.5               # all tied -> exact fallback
+    x = view.float().cpu().numpy()
+    tok, lp, lse, fb = P.row_lse_topm(view, M, kernel="split")
     torch.cuda.synchronize()
     _check_rows(x, M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
 

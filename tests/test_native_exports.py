@@ -23,7 +23,7 @@ def lib():
 
 def header_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^int\s+(vs_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|size_t)\s+(vs_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_bound_exports():

@@ -1,6 +1,6 @@
 """Standalone K1 timing / ncu driver: R rows x |V| logits (log-like values).
 
-    python tools/prof_k1.py [R] [V] [M] [f32|bf16] [--noflush]
+    python tools/prof_k1.py [R] [V] [M] [f32|bf16] [--noflush] [--legacy]
 
 Outputs are pre-allocated and K1 is launched through the C-ABI directly, so
 the CUDA events bracket only the kernel (an L2-flush kernel runs before each
@@ -35,9 +35,20 @@ code = N.VS_DTYPE_F32 if f32 else N.VS_DTYPE_BF16
 stream = torch.cuda.current_stream().cuda_stream
 
 
+legacy = "--legacy" in sys.argv
+nbytes = int(lib.vs_row_lse_topm_ws_bytes(R, V, code))
+ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device="cuda")
+
+
 def launch():
-    N.check(lib.vs_row_lse_topm(x.data_ptr(), code, x.stride(0), V, M, R, None, R, tok.data_ptr(),
-                                lp.data_ptr(), lse.data_ptr(), fb.data_ptr(), stream), "k1")
+    if legacy:
+        N.check(lib.vs_row_lse_topm(x.data_ptr(), code, x.stride(0), V, M, R, None, R, tok.data_ptr(),
+                                    lp.data_ptr(), lse.data_ptr(), fb.data_ptr(), stream), "k1")
+    else:
+        pin = N.VS_K1_SPLIT if "--split" in sys.argv else 0
+        N.check(lib.vs_row_lse_topm_ws(x.data_ptr(), code | pin, x.stride(0), V, M, R, None, R, tok.data_ptr(),
+                                       lp.data_ptr(), lse.data_ptr(), fb.data_ptr(), ws.data_ptr(),
+                                       ws.numel(), stream), "k1")
 
 
 ts = []
