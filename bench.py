@@ -229,6 +229,55 @@ def engines_comparison(reps: int = 3):
     return out
 
 
+def decoder_leg(w, n_inputs: int, reps: int = 2):
+    """BASELINE.json configs[3] with its model: the same VarStream search
+    (k=50, n=128, M=5, δ=1.5, ε=1/6) scoring rows with a random-init
+    transformer-big decoder (6+6 layers, d=1024, FFN 4096, 16 heads,
+    |V|=42024, bf16; decoder.GraphedTransformerScorer).  Synchronous driver
+    (one status read per step), one CUDA-graph replay per decoder step.
+    Inputs: n_inputs taken evenly strided from the workload's length-sorted
+    corpus, so the length mix is the workload's."""
+    import torch
+
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary
+    from paper_2010_02164_b200 import _native as N
+    from paper_2010_02164_b200.decoder import GraphedTransformerScorer
+    from paper_2010_02164_b200.engine import SearchEngine
+
+    corpus = _corpus(w)
+    stride = max(1, len(corpus) // n_inputs)
+    sample = corpus[::stride][:n_inputs]
+    vocab = Vocabulary(w["V"], w["sos"], w["eos"])
+    cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                       max_len=w["max_len"])
+    dec = GraphedTransformerScorer(vocab, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0)
+    eng = SearchEngine(cfg, vocab)
+    times, rep = [], None
+    for i in range(reps + 1):  # first decode captures the per-bucket graphs
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, rep = eng.run(sample, dec, admit_mode=N.VS_ADMIT_VARSTREAM, select_mode=N.VS_SELECT_MIN_LT,
+                         flush_enabled=False)
+        e1.record()
+        torch.cuda.synchronize()
+        if i:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.median(times)
+    return {"value": round(len(sample) / t, 2), "unit": "seq/s", "inputs": len(sample),
+            "sample": f"every {stride}th input of the {len(corpus)}-input length-sorted corpus",
+            "ms_per_decode": round(1e3 * t, 2), "timesteps": rep.timesteps,
+            "ms_per_timestep": round(1e3 * t / rep.timesteps, 3),
+            "expansions_per_step": round(rep.expansions_per_step, 1),
+            "model": f"transformer-big 6+6 layers d=1024 ffn=4096 heads=16 |V|={w['V']}, random init "
+                     f"(seed 0), bf16, logits tau={DEC_TAU}, eos_bias={DEC_EOS_BIAS}*len/src_len",
+            "driver": "synchronous (status read per step), decoder step = 1 CUDA-graph replay per row bucket",
+            "graphs": len(dec.graphs)}
+
+
+DEC_TAU, DEC_EOS_BIAS = 6.0, 20.0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -370,6 +419,8 @@ def run_ours(args):
     }
     if rank == 0 and world == 1:
         line["engines_toy_c2"] = engines_comparison()
+    if rank == 0 and world == 1 and args.decoder_inputs > 0:
+        line["decoder_wmt19"] = decoder_leg(w, args.decoder_inputs)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
@@ -419,6 +470,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-per-proc", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decoder-inputs", type=int, default=2000,
+                    help="inputs for the transformer-big decoder leg (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -235,6 +235,21 @@ int vs_hash_encode(const vs_config* cfg, const vs_state* st, uint64_t seed, void
 int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs_hash_params* hp,
                    void* logits, int64_t ld, int32_t R_grid, void* stream);
 
+/* Decode attention over physical rows (decoder scorer).
+ * For each row r < R (R = *d_R when d_R != NULL, else R_host; grid R_grid):
+ *   out[r, h, :] = softmax_t(q[r,h,:] . K[idx[r], t, h, :] * scale) @ V[idx[r], t, h, :]
+ * over t < lens[r].  K/V element (row, t, h, e) lives at
+ * row*row_stride + t*pos_stride + h*head_dim + e (bf16).  With k_new/v_new
+ * (bf16 [R, heads*head_dim], row stride new_ld) position lens[r]-1 is taken from
+ * them and written into the cache first (self-attention append).  head_dim must
+ * be 64, heads <= 16, lens[r] <= 512.  Replaces nothing in the reference (its
+ * scorer is stateless, bb/model.py:78-87); it is the batched scorer's kernel. */
+int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void* v_cache, int64_t row_stride,
+                     int64_t pos_stride, const int32_t* idx, const int32_t* lens, const void* k_new,
+                     const void* v_new, int64_t new_ld, void* out, int64_t out_ld, int32_t heads,
+                     int32_t head_dim, float scale, int32_t R_host, const int32_t* d_R, int32_t R_grid,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,9 +104,13 @@ class TransformerScorer:
             a = self._merge(self._attn(self._split(cq), self._split(ck), self._split(cv), ckeep))
             x = F.layer_norm(x + a @ L["co"].T, (self.d,))
             x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (self.d,))
-        lg = (x[0, -1] @ self.out.T).float() * self.tau
+        lg = self._project(x[0, -1:])[0].float()
         lg[self.vocab.eos] += self.eos_bias * T / len(src_tokens)
         return lg
+
+    def _project(self, h):
+        """Vocab projection (logits before the EOS bias): tau * h @ W_out^T."""
+        return (h @ self.out.T).float() * self.tau
 
     # --------------------------------------------------------- engine protocol
     def bind(self, engine) -> None:
@@ -193,6 +197,157 @@ class TransformerScorer:
         es = kv.element_size()
         if self.record_logits:
             self.copies += int(engine.t["n_copy"].item())
+        N.check(engine.lib.vs_rows_copy(kv.data_ptr(), kv.stride(0) * es, kv.shape[0], kv.stride(1) * es,
+                                        kv.stride(2) * es, engine.t["copy_list"].data_ptr(),
+                                        engine.t["n_copy"].data_ptr(), engine.capacity, engine.stream_ptr),
+                "vs_rows_copy")
+
+
+class GraphedTransformerScorer(TransformerScorer):
+    """WMT-shape decoder scorer (bf16, head_dim 64) for throughput runs.
+
+    Same model as TransformerScorer (weights, post-LN layers, EOS bias), run
+    as one CUDA graph per step-size bucket:
+
+    * self-attention reads each row's prefix in place from the physical-row
+      K/V cache and appends the new position in the same launch
+      (vs_row_attention); cross-attention reads the slot's encoder states in
+      place (no per-step gathers);
+    * the step's row count lives on the device (status[VS_ST_R]); the graph
+      for bucket Rb = roundup(R, 128) masks the padded rows (they write a
+      dummy cache row), so shapes are static and every launch of the decoder
+      step is a single graph replay;
+    * tau is folded into W_out (logits in bf16, the K1 input dtype).
+
+    K4 (after_step) and the encoder refill (on_admit) run outside the graph.
+    """
+
+    BUCKET = 128
+
+    def __init__(self, vocab: Vocabulary, *, d: int = 1024, heads: int = 16, layers: int = 6,
+                 enc_layers: int = 6, ffn: int = 4096, max_src: int = 256, seed: int = 0,
+                 tau: float = 4.0, eos_bias: float = 4.0, device=None, use_graphs: bool = True):
+        if d % heads or d // heads != 64:
+            raise ValueError("GraphedTransformerScorer needs head_dim 64")
+        super().__init__(vocab, d=d, heads=heads, layers=layers, enc_layers=enc_layers, ffn=ffn,
+                         max_src=max_src, seed=seed, tau=tau, eos_bias=eos_bias, dtype=torch.bfloat16,
+                         device=device)
+        self.out_s = (self.out.float() * tau).to(torch.bfloat16).contiguous()
+        self.use_graphs = use_graphs
+        self.graphs = {}
+
+    def _project(self, h):
+        return (h @ self.out_s.T).float()
+
+    def bind(self, engine) -> None:
+        n, k, Lmax = engine.n, engine.k, engine.max_len
+        if Lmax > self.pos.shape[0]:
+            raise ValueError("max_len exceeds the decoder's positions")
+        dev, d = engine.device, self.d
+        key = (id(engine), n, k, Lmax, engine.capacity)
+        if getattr(self, "_bound", None) != key:  # (re)allocate; graphs capture these buffers
+            self.engine = engine
+            rows = n * k + 1  # + one dummy row for padded step rows
+            self.dummy = n * k
+            self.kv = torch.empty(self.nl, 2, rows, Lmax, d, device=dev, dtype=torch.bfloat16)
+            self.enc_kv = torch.zeros(self.nl, 2, n, self.max_src, d, device=dev, dtype=torch.bfloat16)
+            self.enc_len = torch.zeros(n, dtype=torch.int32, device=dev)
+            ld = (self.vocab.size + 7) // 8 * 8
+            self.lg = torch.empty(engine.capacity, ld, device=dev, dtype=torch.bfloat16)
+            self.graphs = {}
+            self.pool = None
+            self._bound = key
+        self.enc_len.zero_()
+        self._corpus_off = engine.t["src_off"].cpu().numpy()
+        self._corpus_tok = engine.t["src_tok"].cpu().numpy()
+
+    def on_admit(self, engine, status) -> None:
+        n = engine.n
+        a0, na = int(status[N.ST_ADMIT0]), int(status[N.ST_NADMIT])
+        slots = torch.tensor(status[N.ST_HDR + 3 * n:N.ST_HDR + 3 * n + na].astype("int64"),
+                             device=engine.device)
+        srcs = [self._corpus_tok[self._corpus_off[i]:self._corpus_off[i + 1]] for i in range(a0, a0 + na)]
+        lens = torch.tensor([len(s_) for s_ in srcs], device=engine.device)
+        S = int(lens.max())
+        if S > self.max_src:
+            raise ValueError("source longer than the encoder's max_src")
+        pad = torch.zeros(na, S, dtype=torch.long)
+        for i, s_ in enumerate(srcs):
+            pad[i, : len(s_)] = torch.from_numpy(s_.astype("int64"))
+        cross = self.encode_sources(pad.to(engine.device), lens)
+        for li, (ck, cv) in enumerate(cross):
+            self.enc_kv[li, 0, slots, :S] = ck
+            self.enc_kv[li, 1, slots, :S] = cv
+        self.enc_len[slots] = lens.to(torch.int32)
+
+    def _row_attn(self, q, kc, vc, idx, lens, knew, vnew, out):
+        lib = self.engine.lib
+        R = q.shape[0]
+        N.check(lib.vs_row_attention(
+            q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), kc.stride(0), kc.stride(1),
+            idx.data_ptr(), lens.data_ptr(), knew.data_ptr() if knew is not None else None,
+            vnew.data_ptr() if vnew is not None else None, knew.stride(0) if knew is not None else 0,
+            out.data_ptr(), out.stride(0), self.h, 64, 1.0 / 8.0, R, None, R,
+            torch.cuda.current_stream(self.device).cuda_stream), "vs_row_attention")
+
+    def _body(self, Rb: int):
+        eng, t, d = self.engine, self.engine.t, self.d
+        Lmax = eng.max_len
+        R = t["status"][N.ST_R]
+        valid = torch.arange(Rb, device=self.device, dtype=torch.int32) < R
+        phys = t["row_phys"][:Rb]
+        phys_kv = torch.where(valid, phys, self.dummy).to(torch.int32)
+        slot = torch.where(valid, t["row_slot"][:Rb], 0).to(torch.int32)
+        ln = torch.where(valid, t["row_len"][:Rb], 1).to(torch.int32)
+        pos = (ln - 1).long()
+        tok = t["hist"].view(-1, Lmax)[torch.where(valid, phys, 0).long(), pos].long()
+        x = self.emb[tok] + self.pos[pos]
+        enc_len = self.enc_len[slot.long()]
+        att = torch.empty(Rb, d, device=self.device, dtype=torch.bfloat16)
+        for li, L in enumerate(self.dec):
+            qkv = x @ L["qkv"].T
+            self._row_attn(qkv[:, :d], self.kv[li, 0], self.kv[li, 1], phys_kv, ln, qkv[:, d:2 * d],
+                       qkv[:, 2 * d:], att)
+            x = F.layer_norm(x + att @ L["o"].T, (d,))
+            cq = x @ L["cq"].T
+            self._row_attn(cq, self.enc_kv[li, 0], self.enc_kv[li, 1], slot, enc_len, None, None, att)
+            x = F.layer_norm(x + att @ L["co"].T, (d,))
+            x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (d,))
+        lg = self.lg[:Rb, : self.vocab.size]
+        torch.matmul(x, self.out_s.T, out=lg)
+        eos = self.vocab.eos
+        src_len = t["slot_src_len"][slot.long()].float()
+        lg[:, eos] = (lg[:, eos].float() + self.eos_bias * ln.float() / src_len).to(torch.bfloat16)
+        return lg
+
+    def logits(self, engine, R):
+        if R is None:
+            raise RuntimeError("GraphedTransformerScorer needs the synchronous driver")
+        if R == 0:
+            return self.lg, N.VS_DTYPE_BF16
+        Rb = min((R + self.BUCKET - 1) // self.BUCKET * self.BUCKET, engine.capacity)
+        if not self.use_graphs:
+            self._body(Rb)
+            return self.lg, N.VS_DTYPE_BF16
+        g = self.graphs.get(Rb)
+        if g is None:
+            s = torch.cuda.Stream(self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                self._body(Rb)  # warm-up (idempotent: same rows, same writes)
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            if self.pool is None:
+                self.pool = torch.cuda.graph_pool_handle()
+            with torch.cuda.graph(g, pool=self.pool):
+                self._body(Rb)
+            self.graphs[Rb] = g
+        g.replay()
+        return self.lg, N.VS_DTYPE_BF16
+
+    def after_step(self, engine, R) -> None:
+        kv = self.kv.view(self.nl * 2, *self.kv.shape[2:])
+        es = kv.element_size()
         N.check(engine.lib.vs_rows_copy(kv.data_ptr(), kv.stride(0) * es, kv.shape[0], kv.stride(1) * es,
                                         kv.stride(2) * es, engine.t["copy_list"].data_ptr(),
                                         engine.t["n_copy"].data_ptr(), engine.capacity, engine.stream_ptr),

@@ -376,3 +376,54 @@ def test_decoder_decisions_match_oracle_replay():
     want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
     assert _events(ev) == _events(oev)
     assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+
+
+def _graphed_decoder_run(use_graphs=True):
+    P, N, SearchEngine, _, _, LseRecorder = _pkg()
+    from paper_2010_02164_b200.decoder import GraphedTransformerScorer
+
+    vocab = P.Vocabulary(500, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=8, epsilon=1 / 4, delta=2.0, max_candidates=3, max_len=24)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(5, 40, 500, mean_len=7.0, clip=30))
+    dec = GraphedTransformerScorer(vocab, d=128, heads=2, layers=2, enc_layers=1, ffn=256, max_src=32,
+                                   seed=4, tau=3.0, eos_bias=4.0, use_graphs=use_graphs)
+    rec = LseRecorder(dec, record_logits=True)
+    ev = []
+    out, rep = P.run_varstream(corpus, rec, cfg, trace=True, on_step=ev.append)
+    return P, vocab, cfg, corpus, dec, rec, ev, out, rep
+
+
+def test_graphed_decoder_matches_cache_free_forward():
+    """The WMT-shape scorer path (bf16, vs_row_attention in place over the
+    physical-row cache with fused append, K4 reorders, CUDA-graph replay per
+    row bucket) reproduces a cache-free bf16 forward of sampled prefixes
+    (bf16 model: tolerance 0.06 + 2% of the logit scale)."""
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _graphed_decoder_run()
+    assert len(dec.graphs) >= 1
+    keys = sorted(rec.logit_table)
+    rng = np.random.default_rng(1)
+    sample = [keys[i] for i in rng.choice(len(keys), size=min(40, len(keys)), replace=False)]
+    sample += sorted(keys, key=lambda kk: -len(kk[1]))[:10]
+    worst = 0.0
+    for iid, toks in sample:
+        want = dec.full_forward(corpus[iid], toks).cpu().numpy()
+        got = rec.logit_table[(iid, toks)]
+        err = float(np.max(np.abs(got - want)))
+        worst = max(worst, err / (0.06 + 0.02 * float(np.max(np.abs(want)))))
+    assert worst <= 1.0, worst
+
+
+def test_graphed_decoder_decisions_match_oracle_replay_and_eager():
+    """Decisions on the graphed decoder's logits are bit-exact vs the oracle
+    replaying the recorded rows; graph replay and eager execution of the same
+    step body give identical outputs."""
+    from oracle.scorers import RecordedRowsScorer
+
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _graphed_decoder_run()
+    cpu = RecordedRowsScorer(vocab.size, vocab.sos, vocab.eos, rec.logit_table, rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    *_, out2, rep2 = _graphed_decoder_run(use_graphs=False)
+    assert [[(c.tokens, c.score) for c in per] for per in out2] == [[(c.tokens, c.score) for c in per] for per in out]
