@@ -19,6 +19,7 @@ _LAZY = {
     "refill_threshold": "engine",
     "DeviceHashScorer": "scorers", "HostScorerAdapter": "scorers", "BatchedScorer": "scorers",
     "run_varstream": "scheduler", "run_varbeam": "scheduler", "run_varfifo": "scheduler",
+    "run_greedy": "scheduler",
     "dispatch_engine": "scheduler", "ENGINES": "scheduler",
     "expand_beam": "search", "row_lse_topm": "search",
 }

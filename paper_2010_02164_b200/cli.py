@@ -23,7 +23,7 @@ from pathlib import Path
 from .core import DecodeConfig, Vocabulary
 from .errors import ConfigError, DataError, InvariantViolation
 
-ENGINES = ("fixed", "varbeam", "varstream", "varfifo", "fixedstream")
+ENGINES = ("greedy", "fixed", "varbeam", "varstream", "varfifo", "fixedstream")
 _DECODE = ("k", "n", "epsilon", "delta", "max_candidates", "max_len", "policy", "capacity",
            "flush_interval", "cost_c0", "cost_c1")
 

@@ -14,11 +14,12 @@ import math
 
 from . import _native as N
 from .core import DecodeConfig, Vocabulary
+from .metrics import CostParams, MetricsReport
 from .engine import SearchEngine
 from .errors import ConfigError
 from .scorers import HostScorerAdapter
 
-ENGINES = ("fixed", "varbeam", "varstream", "varfifo", "fixedstream")
+ENGINES = ("greedy", "fixed", "varbeam", "varstream", "varfifo", "fixedstream")
 _PRUNING_OFF = {"fixed": "varbeam", "fixedstream": "varstream"}
 
 
@@ -66,8 +67,34 @@ def run_varfifo(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on
                 on_step, fast)
 
 
+def run_greedy(corpus, scorer, config: DecodeConfig, *, trace: bool = False):
+    """Greedy decoding of every input (bb/search.py:38-49 greedy_decode via
+    bb/harness.py:222-238 _run_greedy): repeatedly append the argmax token
+    (ties to the lower id) until EOS or max_len.
+
+    The reference decodes one input at a time; here all inputs stream
+    through one device batch as width-1 beams (k=1, M=1, δ=inf, ε-refill with
+    n = config.n * config.k slots), which yields the same candidates
+    (bb tests/test_harness.py:177-182: greedy == width-one fixed).  The
+    MetricsReport keeps the reference's unbatched accounting: one step of one
+    expansion per appended token, effective_len = prefix length
+    (bb/harness.py:235-236)."""
+    n = max(1, min(N.VS_MAX_SLOTS, config.n * config.k))
+    g = DecodeConfig(k=1, n=n, epsilon=config.epsilon, delta=math.inf, max_candidates=1,
+                     max_len=config.max_len, cost_c0=config.cost_c0, cost_c1=config.cost_c1)
+    outs, _ = run_varstream(corpus, scorer, g)
+    report = MetricsReport.new(trace=trace)
+    cost = CostParams(config.cost_c0, config.cost_c1)
+    for per in outs:
+        for length in range(1, len(per[0].tokens)):
+            report.record_step(1, length, cost)
+    return [[per[0]] for per in outs], report
+
+
 def dispatch_engine(engine: str, corpus, scorer, config: DecodeConfig, *, trace: bool = False):
-    """bb/harness.py:241-260 (greedy is out of scope for the device path)."""
+    """bb/harness.py:241-260."""
+    if engine == "greedy":
+        return run_greedy(corpus, scorer, config, trace=trace)
     runner = {"fixed": run_varbeam, "varbeam": run_varbeam, "varstream": run_varstream,
               "fixedstream": run_varstream, "varfifo": run_varfifo}.get(engine)
     if runner is None:

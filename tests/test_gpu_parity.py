@@ -257,6 +257,27 @@ def test_engine_with_reference_scorer_matches_oracle_events(name):
     assert rep.simulated_cost == wrep.simulated_cost
 
 
+def test_greedy_engine_matches_reference_greedy_decode():
+    """dispatch_engine("greedy") (batched width-1 beams on the device) gives
+    the candidates of bb/search.py:38-49 greedy_decode for every input, and
+    the metrics of the reference's unbatched accounting (bb/harness.py:222-238)."""
+    P, *_ = _pkg()
+    fx = RUNS["c1_varstream_eps0.1667"]
+    s = fx["scorer"]
+    base = SeededHashScorerCPU(s["vocab_size"], s["sos"], s["eos"], s["seed"], s["eos_bias"])
+    d = fx["config"]
+    cfg = P.DecodeConfig(k=d["k"], n=d["n"], max_len=d["max_len"])
+    corpus = [tuple(x) for x in fx["corpus"]][:80]
+    vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
+    out, rep = P.dispatch_engine("greedy", corpus, _RefVocabScorer(base, vocab), cfg, trace=True)
+    ref = _F32Rows(base)
+    want = [O.greedy_decode(ref.encode(x, i), ref, cfg.max_len) for i, x in enumerate(corpus)]
+    assert [[(c.tokens, c.score) for c in per] for per in out] == [[(c.tokens, c.score)] for c in want]
+    steps = sum(len(c.tokens) - 1 for c in want)
+    assert rep.timesteps == steps and rep.candidate_expansions == steps
+    assert [(r[1], r[2]) for r in rep.per_step_trace] == [(1, L) for c in want for L in range(1, len(c.tokens))]
+
+
 HASH_CASES = [
     # name, V, k, n, M, delta, max_len, eps, N, dtype, scale, power, eos_bias[, policy]
     ("toy_c1", 1000, 5, 32, 3, 1.5, 48, 1 / 6, 160, "bf16", 8.0, 1, 6.0),
