@@ -17,7 +17,7 @@ src = ROOT / "gpurun_out"
 dst = ROOT / "profiles" / rnd
 dst.mkdir(parents=True, exist_ok=True)
 summary = {}
-for rep in ("k1_fullwidth", "k1_decode", "step_kernels"):
+for rep in ("k1_fullwidth", "k1_decode", "step_kernels", "k1t_fw", "k1t_573"):
     p = src / f"{rep}.ncu-rep"
     if not p.exists():
         continue
@@ -31,7 +31,19 @@ for rep in ("k1_fullwidth", "k1_decode", "step_kernels"):
     # per-instruction stall summary (top-level)
     out = subprocess.run(["ncu", "-i", str(p), "--page", "details", "--csv"], capture_output=True, text=True).stdout
     (dst / f"{rep}_details.csv").write_text(out)
-if (src / "launches_decode.csv").exists():
+    if rep.startswith("k1t"):  # SASS-region breakdown of the split-row kernel
+        units = {"k1t_fw": 134400, "k1t_573": 12033}[rep]
+        out = subprocess.run([sys.executable, str(ROOT / "tools" / "sass_hot.py"), str(p), str(units), "30"],
+                             capture_output=True, text=True).stdout
+        (dst / f"{rep}_sass_regions.txt").write_text(out)
+for name in ("launches_decode", "dec_launches"):
+    if not (src / f"{name}.csv").exists():
+        continue
+    shutil.copy(src / f"{name}.csv", dst / f"{name}.csv")
+    out = subprocess.run([sys.executable, str(ROOT / "tools" / "launch_summary.py"), str(src / f"{name}.csv")],
+                         capture_output=True, text=True).stdout
+    (dst / f"{name}_summary.txt").write_text(out)
+if False:
     shutil.copy(src / "launches_decode.csv", dst / "launches_decode.csv")
     out = subprocess.run([sys.executable, str(ROOT / "tools" / "launch_summary.py"), str(src / "launches_decode.csv")],
                          capture_output=True, text=True).stdout
