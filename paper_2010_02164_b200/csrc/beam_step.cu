@@ -67,6 +67,7 @@ __device__ __forceinline__ int block_prefix(bool pred, int* wsm, int* total) {
 }
 
 __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows) {
+  VS_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.x;
   if (b >= st.status[VS_ST_NSEL]) return;
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
 // excluded element can tie the 2k-th sum through fp64 merging of distinct
 // logps (flags InvariantViolation otherwise; needs |score| ~ 2^29 |dlogp|).
 __global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg, vs_state st, int M_rows) {
+  VS_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem[];
   const int b = blockIdx.x;
   if (b >= st.status[VS_ST_NSEL]) return;
@@ -628,7 +630,7 @@ extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
         return VS_ERR_CUDA;
       configured_i = smem;
     }
-    vs::beam_step_immediate_kernel<<<cfg->n, vs::NT2, smem, strm>>>(*cfg, *st, M_rows);
+    vs::vs_launch(vs::beam_step_immediate_kernel, dim3(cfg->n), dim3(vs::NT2), smem, strm, *cfg, *st, M_rows);
     VS_CUDA_RET();
   }
   if (cfg->policy != VS_POLICY_DEFERRED) return VS_ERR_CONFIG;
@@ -644,6 +646,6 @@ extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
       return VS_ERR_CUDA;
     configured = smem;
   }
-  vs::beam_step_kernel<<<cfg->n, vs::NT2, smem, strm>>>(*cfg, *st, M_rows);
+  vs::vs_launch(vs::beam_step_kernel, dim3(cfg->n), dim3(vs::NT2), smem, strm, *cfg, *st, M_rows);
   VS_CUDA_RET();
 }

@@ -103,7 +103,37 @@ __device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2
   s = a + b;
 }
 
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// Every kernel starts with VS_PDL_ENTRY(): wait until the preceding kernel in
+// the stream has completed (its writes visible), then allow the next one to
+// be launched, so launch latency and the next grid's ramp overlap this
+// kernel's tail.  Kernels are launched with vs_launch (cudaLaunchKernelEx +
+// programmatic stream serialization; VS_PDL=0 disables it).
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t vs_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace vs
+
+#define VS_PDL_ENTRY() ::vs::pdl_entry()
 
 #define VS_CUDA_RET()                                              \
   do {                                                             \

@@ -13,6 +13,7 @@ namespace vs {
 namespace {
 
 __global__ void hash_encode_kernel(vs_config cfg, vs_state st, uint64_t seed) {
+  VS_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int nadm = st.status[VS_ST_NADMIT];
   if (i >= nadm) return;
@@ -53,6 +54,7 @@ __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __
 template <typename T>
 __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_state st, vs_hash_params hp,
                                                           T* __restrict__ logits, int64_t ld, int cols) {
+  VS_PDL_ENTRY();
   const int R = st.status[VS_ST_R];
   const int V = cfg.vocab_size;
   for (int w = blockIdx.x; w < R * cols; w += gridDim.x) {
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_stat
 extern "C" int vs_hash_encode(const vs_config* cfg, const vs_state* st, uint64_t seed, void* stream) {
   if (!cfg || !st) return VS_ERR_CONFIG;
   const int n = cfg->n;
-  vs::hash_encode_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(*cfg, *st, seed);
+  vs::vs_launch(vs::hash_encode_kernel, dim3((n + 127) / 128), dim3(128), 0, static_cast<cudaStream_t>(stream), *cfg, *st, seed);
   VS_CUDA_RET();
 }
 
@@ -112,9 +114,9 @@ extern "C" int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs
   const int grid = (int)(need < (long)sms * 8 ? need : (long)sms * 8);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (hp->dtype == VS_DTYPE_F32)
-    vs::hash_logits_kernel<float><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<float*>(logits), ld, cols);
+    vs::vs_launch(vs::hash_logits_kernel<float>, dim3(grid), dim3(256), 0, s, *cfg, *st, *hp, static_cast<float*>(logits), ld, cols);
   else if (hp->dtype == VS_DTYPE_BF16)
-    vs::hash_logits_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(*cfg, *st, *hp, static_cast<__nv_bfloat16*>(logits), ld, cols);
+    vs::vs_launch(vs::hash_logits_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, *cfg, *st, *hp, static_cast<__nv_bfloat16*>(logits), ld, cols);
   else
     return VS_ERR_CONFIG;
   VS_CUDA_RET();

@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(256) rows_copy_kernel(unsigned char* __restric
                                                         int64_t row_stride, int64_t pos_bytes,
                                                         const int32_t* __restrict__ copy_list,
                                                         const int32_t* __restrict__ n_copy) {
+  VS_PDL_ENTRY();
   const int c = blockIdx.x;
   if (c >= *n_copy) return;
   const int plane = blockIdx.y;
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(unsigned char* __rest
                                                            int64_t src_stride, int64_t bytes,
                                                            const int32_t* __restrict__ slots,
                                                            const int32_t* __restrict__ d_count) {
+  VS_PDL_ENTRY();
   const int i = blockIdx.x;
   if (d_count && i >= *d_count) return;
   const unsigned char* s = src + (int64_t)i * src_stride;
@@ -65,7 +67,7 @@ extern "C" int vs_rows_copy(void* base, int64_t plane_stride_bytes, int32_t plan
     return VS_ERR_CONFIG;
   if (max_copies <= 0) return VS_OK;
   dim3 grid(max_copies, planes);
-  vs::rows_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  vs::vs_launch(vs::rows_copy_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<unsigned char*>(base), plane_stride_bytes, planes, row_stride_bytes, pos_bytes,
       copy_list, n_copy);
   VS_CUDA_RET();
@@ -76,7 +78,7 @@ extern "C" int vs_scatter_rows(void* dst, int64_t dst_stride_bytes, const void* 
                                const int32_t* d_count, int32_t count_max, void* stream) {
   if (!dst || !src || !slots || bytes < 0) return VS_ERR_CONFIG;
   if (count_max <= 0 || bytes == 0) return VS_OK;
-  vs::scatter_rows_kernel<<<count_max, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  vs::vs_launch(vs::scatter_rows_kernel, dim3(count_max), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<unsigned char*>(dst), dst_stride_bytes, static_cast<const unsigned char*>(src),
       src_stride_bytes, bytes, slots, d_count);
   VS_CUDA_RET();

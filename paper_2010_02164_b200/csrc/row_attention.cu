@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
     const int* __restrict__ lens, const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
     int64_t new_ld, __nv_bfloat16* __restrict__ out, int64_t out_ld, int H, float scale, int R_host,
     const int* __restrict__ d_R) {
+  VS_PDL_ENTRY();
   const int r = blockIdx.x;
   const int R = d_R ? *d_R : R_host;
   if (r >= R) return;
@@ -166,7 +167,7 @@ extern "C" int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void
       R_grid < 0 || ((k_new == nullptr) != (v_new == nullptr)))
     return VS_ERR_CONFIG;
   if (R_grid == 0) return VS_OK;
-  vs::row_attention_kernel<<<R_grid, 32 * heads, 0, static_cast<cudaStream_t>(stream)>>>(
+  vs::vs_launch(vs::row_attention_kernel, dim3(R_grid), dim3(32 * heads), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const __nv_bfloat16*>(q), q_ld, static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache), row_stride, pos_stride, idx, lens,
       static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new), new_ld,

@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
     int* __restrict__ fb_count, int normalized, int sms, int flush_min, int pf_batches,
     int warps_per_sm) {
+  VS_PDL_ENTRY();
   constexpr int VEC = 16 / sizeof(T);
   __shared__ uint64_t sbuf[WPC][CAPW];
   __shared__ uint64_t ssel[WPC][VS_MAX_M];
@@ -565,7 +566,7 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
   }
   const T* p = static_cast<const T*>(logits);
 #define VS_K1_LAUNCH(U_, B_)                                                                            \
-  row_lse_topm_warp_kernel<T, U_, B_><<<grid, WPC * 32, 0, st>>>(p, ld, V, M, R_host, d_R, top_tok, \
+  vs::vs_launch(row_lse_topm_warp_kernel<T, U_, B_>, dim3(grid), dim3(WPC * 32), 0, st, p, ld, V, M, R_host, d_R, top_tok, \
                                                                  top_logp, row_lse, fb, norm, sms, flush_min, pf, \
                                                                  ctas_per_sm * WPC)
   switch (variant) {
@@ -585,6 +586,17 @@ template <typename T>
 int launch_tma(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int R_grid,
                int* top_tok, float* top_logp, float* row_lse, int* fb, int norm, void* ws, size_t ws_bytes,
                cudaStream_t st);
+}  // namespace vs
+
+namespace vs {
+bool pdl_enabled() {
+  static int e = -1;
+  if (e < 0) {
+    const char* v = getenv("VS_PDL");
+    e = v ? atoi(v) : 1;
+  }
+  return e != 0;
+}
 }  // namespace vs
 
 extern "C" int vs_version(void) { return 3; }

@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(NW * 32, 5) row_lse_topm_tma_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
     int* __restrict__ fb_count, int normalized, unsigned char* __restrict__ ws, int flush_min, int dbg) {
+  VS_PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   WarpSmem<NS>* all = reinterpret_cast<WarpSmem<NS>*>(smem_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -838,7 +839,7 @@ int launch_tma(const void* logits, int64_t ld, int V, int M, int R_host, const i
       if (fit < 1) fit = 1;                                                                          \
     }                                                                                                \
     const int grid = sms * (ctas > 0 ? min(ctas, fit) : fit);                                        \
-    kern<<<grid, tk::NW * 32, smem, st>>>(x, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm, \
+    vs::vs_launch(kern, dim3(grid), dim3(tk::NW * 32), smem, st, x, ld, V, M, R_host, d_R, top_tok, top_logp, row_lse, fb, norm, \
                                           static_cast<unsigned char*>(ws), flush_min, dbg);               \
   } while (0)
   switch (ns) {

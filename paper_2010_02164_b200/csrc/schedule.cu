@@ -64,6 +64,7 @@ __device__ __forceinline__ int block_min(int v, int* scratch) {
 
 __global__ void __launch_bounds__(NT3) schedule_kernel(vs_config cfg, vs_state st, int N, int first,
                                                        int do_remove, int admit_mode, int select_mode) {
+  VS_PDL_ENTRY();
   __shared__ int wsum[33];
   __shared__ int live_s[VS_MAX_SLOTS];
   __shared__ int order_s[VS_MAX_SLOTS];
@@ -342,7 +343,7 @@ extern "C" int vs_schedule(const vs_config* cfg, const vs_state* st, int32_t N, 
   if (!cfg || !st || cfg->n < 1 || cfg->n > VS_MAX_SLOTS || cfg->k < 1 || cfg->k > VS_MAX_K ||
       N < 1 || cfg->capacity < cfg->k)
     return VS_ERR_CONFIG;
-  vs::schedule_kernel<<<1, vs::NT3, 0, static_cast<cudaStream_t>(stream)>>>(
+  vs::vs_launch(vs::schedule_kernel, dim3(1), dim3(vs::NT3), 0, static_cast<cudaStream_t>(stream), 
       *cfg, *st, N, first_call, do_remove, admit_mode, select_mode);
   VS_CUDA_RET();
 }
