@@ -250,6 +250,25 @@ int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void* v_cache, 
                      int32_t head_dim, float scale, int32_t R_host, const int32_t* d_R, int32_t R_grid,
                      void* stream);
 
+/* K5  proj_lse_topM — the decoder's vocab projection on tcgen05 tensor cores
+ * with K1 fused into the epilogue (csrc/proj_topm.cu).  For rows r < R
+ * (R = *d_R when d_R != NULL, else R_host; R_grid bounds R and sizes the TMA
+ * map of H):
+ *   x[r, v] = bf16(H[r, :] . W[v, :]), x[r, eos] = bf16(x[r, eos] + eos_add[r])
+ *   lse[r], top-M by (logp desc, token asc) — K1's contract on x.
+ * H: bf16 [R_grid, K] (row stride ldh), W: bf16 [V, K] (row stride ldw), K a
+ * multiple of 64, M <= 8, |V| <= 65536.  logits (bf16 [R, ldo], required)
+ * receives x: the merge reads only the few 128-column sub-tiles that can hold
+ * a row's top-M, and the exact fallback reads the row.  Workspace:
+ * vs_proj_lse_topm_ws_bytes(R_grid, V) bytes (no zeroing needed).  Replaces the vocab GEMM + bb/model.py:216-217 +
+ * bb/search.py:63-73. */
+int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64_t ldw, int32_t R_host,
+                     const int32_t* d_R, int32_t R_grid, int32_t K, int32_t V, int32_t M, int32_t eos,
+                     const float* eos_add, void* logits, int64_t ldo, int32_t* top_tok, float* top_logp,
+                     float* row_lse, int32_t* fallback_count, void* workspace, size_t workspace_bytes,
+                     void* stream);
+size_t vs_proj_lse_topm_ws_bytes(int32_t R_grid, int32_t V);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,7 +60,8 @@ class VsHashParams(C.Structure):
 
 # Every symbol include/varstream.h declares (checked by tests/test_native_exports.py).
 EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step", "vs_schedule", "vs_rows_copy",
-           "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention")
+           "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention",
+           "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes")
 
 _lib = None
 
@@ -86,6 +87,9 @@ def load_library(path: Path | None = None) -> C.CDLL:
         "vs_rows_copy": ([vp, i64, i32, i64, i64, vp, vp, i32, vp], i32),
         "vs_scatter_rows": ([vp, i64, vp, i64, i64, vp, vp, i32, vp], i32),
         "vs_hash_encode": ([C.POINTER(VsConfig), C.POINTER(VsState), u64, vp], i32),
+        "vs_proj_lse_topm": ([vp, i64, vp, i64, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, vp, vp, vp,
+                              vp, C.c_size_t, vp], i32),
+        "vs_proj_lse_topm_ws_bytes": ([i32, i32], C.c_size_t),
         "vs_row_attention": ([vp, i64, vp, vp, i64, i64, vp, vp, vp, vp, i64, vp, i64, i32, i32, C.c_float,
                               i32, vp, i32, vp], i32),
         "vs_hash_logits": ([C.POINTER(VsConfig), C.POINTER(VsState), C.POINTER(VsHashParams), vp,

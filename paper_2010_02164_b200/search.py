@@ -69,6 +69,32 @@ def row_lse_topm(logits: torch.Tensor, M: int, *, normalized: bool = False, lega
     return tok, lp, lse, fb
 
 
+def proj_lse_topm(h: torch.Tensor, w: torch.Tensor, M: int, *, eos: int = -1, eos_add=None):
+    """K5 (tcgen05 vocab projection + fused K1): logits = bf16(h @ w^T) with the
+    EOS bias, and K1's outputs on them.  h bf16 [R, K], w bf16 [V, K].
+    Returns (tokens [R, M], logp [R, M], lse [R], fallbacks, logits [R, V])."""
+    if h.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or h.shape[1] != w.shape[1]:
+        raise ValueError("h [R, K] and w [V, K] must be bf16 with the same K")
+    R, K = h.shape
+    V = w.shape[0]
+    dev = h.device
+    tok = torch.empty((R, M), dtype=torch.int32, device=dev)
+    lp = torch.empty((R, M), dtype=torch.float32, device=dev)
+    lse = torch.empty((R,), dtype=torch.float32, device=dev)
+    fb = torch.zeros((1,), dtype=torch.int32, device=dev)
+    ld = (V + 7) // 8 * 8
+    lg = torch.empty((R, ld), dtype=torch.bfloat16, device=dev)
+    lib = N.load_library()
+    ws = torch.empty(max(int(lib.vs_proj_lse_topm_ws_bytes(R, V)), 256), dtype=torch.uint8, device=dev)
+    ea = eos_add.float().contiguous() if eos_add is not None else None
+    N.check(lib.vs_proj_lse_topm(h.data_ptr(), h.stride(0), w.data_ptr(), w.stride(0), R, None, R, K, V, M, eos,
+                                 ea.data_ptr() if ea is not None else None,
+                                 lg.data_ptr(), ld, tok.data_ptr(), lp.data_ptr(),
+                                 lse.data_ptr(), fb.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 torch.cuda.current_stream(dev).cuda_stream), "vs_proj_lse_topm")
+    return tok, lp, lse, fb, lg[:, :V]
+
+
 def _load_beam(eng: SearchEngine, beam: Beam) -> int:
     """Write one beam into slot 0 of a 1-slot engine; returns its active width."""
     k, L = eng.k, eng.max_len

@@ -448,3 +448,29 @@ def test_graphed_decoder_decisions_match_oracle_replay_and_eager():
     assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
     *_, out2, rep2 = _graphed_decoder_run(use_graphs=False)
     assert [[(c.tokens, c.score) for c in per] for per in out2] == [[(c.tokens, c.score) for c in per] for per in out]
+
+
+@pytest.mark.parametrize("R,V,M", [(1, 1000, 5), (37, 5003, 5), (300, 42024, 5), (129, 2048, 8)])
+def test_proj_topm_tcgen05_matches_oracle(R, V, M):
+    """K5: tcgen05 vocab projection with the fused K1 epilogue.  Its bf16
+    logits match a torch fp32 GEMM within one bf16 ulp (different accumulation
+    order), and every top-M decision/logp is bit-exact vs the oracle on the
+    logits it wrote (K1's contract), with lse within 1e-5 of fp64."""
+    from paper_2010_02164_b200.search import proj_lse_topm
+
+    torch.manual_seed(R + V)
+    K = 1024
+    h = (torch.randn(R, K, device="cuda") * 0.5).to(torch.bfloat16)
+    w = (torch.randn(V, K, device="cuda") / 16).to(torch.bfloat16)
+    eos = 2
+    eos_add = torch.rand(R, device="cuda") * 3
+    tok, lp, lse, fb, lg = proj_lse_topm(h, w, M, eos=eos, eos_add=eos_add)
+    torch.cuda.synchronize()
+    ref = (h.float() @ w.float().T)
+    ref_bf = ref.to(torch.bfloat16).float()
+    ref_bf[:, eos] = (ref_bf[:, eos] + eos_add).to(torch.bfloat16).float()
+    got = lg.float()
+    ulp = ref_bf.abs().clamp_min(1e-3) * 2.0 ** -7
+    assert bool(((got - ref_bf).abs() <= ulp + 1e-6).all()), float((got - ref_bf).abs().max())
+    x = got.cpu().numpy()
+    _check_rows(x, M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
