@@ -229,7 +229,7 @@ def engines_comparison(reps: int = 3):
     return out
 
 
-def decoder_leg(w, n_inputs: int, reps: int = 2):
+def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False):
     """BASELINE.json configs[3] with its model: the same VarStream search
     (k=50, n=128, M=5, δ=1.5, ε=1/6) scoring rows with a random-init
     transformer-big decoder (6+6 layers, d=1024, FFN 4096, 16 heads,
@@ -250,7 +250,8 @@ def decoder_leg(w, n_inputs: int, reps: int = 2):
     vocab = Vocabulary(w["V"], w["sos"], w["eos"])
     cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
                        max_len=w["max_len"])
-    dec = GraphedTransformerScorer(vocab, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0)
+    dec = GraphedTransformerScorer(vocab, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0,
+                                   fused_head=fused_head)
     eng = SearchEngine(cfg, vocab)
     times, rep = [], None
     for i in range(reps + 1):  # first decode captures the per-bucket graphs
@@ -272,6 +273,8 @@ def decoder_leg(w, n_inputs: int, reps: int = 2):
             "model": f"transformer-big 6+6 layers d=1024 ffn=4096 heads=16 |V|={w['V']}, random init "
                      f"(seed 0), bf16, logits tau={DEC_TAU}, eos_bias={DEC_EOS_BIAS}*len/src_len",
             "driver": "synchronous (status read per step), decoder step = 1 CUDA-graph replay per row bucket",
+            "head": "K5 tcgen05 projection + fused log-softmax/top-M" if fused_head
+                    else "cuBLAS projection + K1",
             "graphs": len(dec.graphs)}
 
 
@@ -423,6 +426,7 @@ def run_ours(args):
         line["engines_toy_c2"] = engines_comparison()
     if rank == 0 and world == 1 and args.decoder_inputs > 0:
         line["decoder_wmt19"] = decoder_leg(w, args.decoder_inputs)
+        line["decoder_wmt19_k5"] = decoder_leg(w, args.decoder_inputs, fused_head=True)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",

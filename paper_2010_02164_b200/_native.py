@@ -18,6 +18,9 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvarstream.so"
 VS_OK, VS_ERR_CONFIG, VS_ERR_INVARIANT, VS_ERR_CUDA = 0, -1, -3, -4
 VS_DTYPE_F32, VS_DTYPE_BF16, VS_ROWS_NORMALIZED = 0, 1, 0x100
 VS_K1_SPLIT, VS_K1_WARP = 0x200, 0x400  # pin the K1 kernel (vs_row_lse_topm_ws)
+# BatchedScorer.logits may return this code: the scorer already produced K1's
+# outputs (top_tok / top_logp / row_lse) for the step, e.g. with the fused K5 head
+VS_K1_DONE = -1
 VS_POLICY_DEFERRED, VS_POLICY_IMMEDIATE = 0, 1
 VS_ADMIT_NONE, VS_ADMIT_VARSTREAM, VS_ADMIT_VARBEAM, VS_ADMIT_VARFIFO = -1, 0, 1, 2
 VS_SELECT_MIN_LT, VS_SELECT_FIFO, VS_SELECT_ALL = 0, 1, 2

@@ -226,7 +226,8 @@ class GraphedTransformerScorer(TransformerScorer):
 
     def __init__(self, vocab: Vocabulary, *, d: int = 1024, heads: int = 16, layers: int = 6,
                  enc_layers: int = 6, ffn: int = 4096, max_src: int = 256, seed: int = 0,
-                 tau: float = 4.0, eos_bias: float = 4.0, device=None, use_graphs: bool = True):
+                 tau: float = 4.0, eos_bias: float = 4.0, device=None, use_graphs: bool = True,
+                 fused_head: bool = False):
         if d % heads or d // heads != 64:
             raise ValueError("GraphedTransformerScorer needs head_dim 64")
         super().__init__(vocab, d=d, heads=heads, layers=layers, enc_layers=enc_layers, ffn=ffn,
@@ -234,6 +235,7 @@ class GraphedTransformerScorer(TransformerScorer):
                          device=device)
         self.out_s = (self.out.float() * tau).to(torch.bfloat16).contiguous()
         self.use_graphs = use_graphs
+        self.fused_head = fused_head  # K5: tcgen05 vocab projection with K1 fused into the epilogue
         self.graphs = {}
 
     def _project(self, h):
@@ -254,6 +256,9 @@ class GraphedTransformerScorer(TransformerScorer):
             self.enc_len = torch.zeros(n, dtype=torch.int32, device=dev)
             ld = (self.vocab.size + 7) // 8 * 8
             self.lg = torch.empty(engine.capacity, ld, device=dev, dtype=torch.bfloat16)
+            if self.fused_head:
+                nb = int(engine.lib.vs_proj_lse_topm_ws_bytes(engine.capacity, self.vocab.size))
+                self.k5_ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
             self.graphs = {}
             self.pool = None
             self._bound = key
@@ -314,21 +319,32 @@ class GraphedTransformerScorer(TransformerScorer):
             x = F.layer_norm(x + att @ L["co"].T, (d,))
             x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (d,))
         lg = self.lg[:Rb, : self.vocab.size]
-        torch.matmul(x, self.out_s.T, out=lg)
         eos = self.vocab.eos
         src_len = t["slot_src_len"][slot.long()].float()
+        if self.fused_head:  # K5: projection + EOS bias + K1 in two launches
+            eos_add = (self.eos_bias * ln.float() / src_len).contiguous()
+            x = x.contiguous()
+            N.check(eng.lib.vs_proj_lse_topm(
+                x.data_ptr(), x.stride(0), self.out_s.data_ptr(), self.out_s.stride(0), Rb, None, Rb, d,
+                self.vocab.size, eng.m_rows, eos, eos_add.data_ptr(), self.lg.data_ptr(), self.lg.stride(0),
+                t["top_tok"].data_ptr(), t["top_logp"].data_ptr(), t["row_lse"].data_ptr(),
+                t["fallbacks"].data_ptr(), self.k5_ws.data_ptr(), self.k5_ws.numel(),
+                torch.cuda.current_stream(self.device).cuda_stream), "vs_proj_lse_topm")
+            return lg
+        torch.matmul(x, self.out_s.T, out=lg)
         lg[:, eos] = (lg[:, eos].float() + self.eos_bias * ln.float() / src_len).to(torch.bfloat16)
         return lg
 
     def logits(self, engine, R):
         if R is None:
             raise RuntimeError("GraphedTransformerScorer needs the synchronous driver")
+        code = N.VS_K1_DONE if self.fused_head else N.VS_DTYPE_BF16
         if R == 0:
             return self.lg, N.VS_DTYPE_BF16
         Rb = min((R + self.BUCKET - 1) // self.BUCKET * self.BUCKET, engine.capacity)
         if not self.use_graphs:
             self._body(Rb)
-            return self.lg, N.VS_DTYPE_BF16
+            return self.lg, code
         g = self.graphs.get(Rb)
         if g is None:
             s = torch.cuda.Stream(self.device)
@@ -343,7 +359,7 @@ class GraphedTransformerScorer(TransformerScorer):
                 self._body(Rb)
             self.graphs[Rb] = g
         g.replay()
-        return self.lg, N.VS_DTYPE_BF16
+        return self.lg, code
 
     def after_step(self, engine, R) -> None:
         kv = self.kv.view(self.nl * 2, *self.kv.shape[2:])

@@ -222,7 +222,8 @@ class SearchEngine:
         if phase == "stream" and st[N.ST_NADMIT] > 0:
             scorer.on_admit(self, st)
         logits, code = scorer.logits(self, R)
-        self.row_topm(logits, code, R, R)
+        if code != N.VS_K1_DONE:
+            self.row_topm(logits, code, R, R)
         self.beam_step()
         scorer.after_step(self, R)
 
@@ -323,7 +324,8 @@ class SearchEngine:
             if k1_events is not None:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            self.row_topm(logits, code, 0, cap, d_R)
+            if code != N.VS_K1_DONE:
+                self.row_topm(logits, code, 0, cap, d_R)
             if k1_events is not None:
                 e1.record(stream)
                 k1_events.append((e0, e1))

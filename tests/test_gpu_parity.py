@@ -399,7 +399,7 @@ def test_decoder_decisions_match_oracle_replay():
     assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
 
 
-def _graphed_decoder_run(use_graphs=True):
+def _graphed_decoder_run(use_graphs=True, fused_head=False):
     P, N, SearchEngine, _, _, LseRecorder = _pkg()
     from paper_2010_02164_b200.decoder import GraphedTransformerScorer
 
@@ -407,7 +407,7 @@ def _graphed_decoder_run(use_graphs=True):
     cfg = P.DecodeConfig(k=6, n=8, epsilon=1 / 4, delta=2.0, max_candidates=3, max_len=24)
     corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(5, 40, 500, mean_len=7.0, clip=30))
     dec = GraphedTransformerScorer(vocab, d=128, heads=2, layers=2, enc_layers=1, ffn=256, max_src=32,
-                                   seed=4, tau=3.0, eos_bias=4.0, use_graphs=use_graphs)
+                                   seed=4, tau=3.0, eos_bias=4.0, use_graphs=use_graphs, fused_head=fused_head)
     rec = LseRecorder(dec, record_logits=True)
     ev = []
     out, rep = P.run_varstream(corpus, rec, cfg, trace=True, on_step=ev.append)
@@ -474,3 +474,22 @@ def test_proj_topm_tcgen05_matches_oracle(R, V, M):
     assert bool(((got - ref_bf).abs() <= ulp + 1e-6).all()), float((got - ref_bf).abs().max())
     x = got.cpu().numpy()
     _check_rows(x, M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
+
+
+def test_graphed_decoder_with_fused_k5_head_matches_oracle_replay():
+    """The decoder with the tcgen05 vocab projection + fused K1 (K5) inside the
+    step graph: every decision bit-exact vs the oracle replaying the logits K5
+    wrote and the lse it exported; logits match the cache-free forward."""
+    from oracle.scorers import RecordedRowsScorer
+
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _graphed_decoder_run(fused_head=True)
+    cpu = RecordedRowsScorer(vocab.size, vocab.sos, vocab.eos, rec.logit_table, rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    keys = sorted(rec.logit_table)
+    for iid, toks in keys[:: max(1, len(keys) // 30)]:
+        want_l = dec.full_forward(corpus[iid], toks).cpu().numpy()
+        got = rec.logit_table[(iid, toks)]
+        assert np.max(np.abs(got - want_l)) <= 0.06 + 0.02 * float(np.max(np.abs(want_l)))
