@@ -242,7 +242,7 @@ int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs_hash_param
  * row*row_stride + t*pos_stride + h*head_dim + e (bf16).  With k_new/v_new
  * (bf16 [R, heads*head_dim], row stride new_ld) position lens[r]-1 is taken from
  * them and written into the cache first (self-attention append).  head_dim must
- * be 64, heads <= 16, lens[r] <= 512.  Replaces nothing in the reference (its
+ * be 64, heads a multiple of 4, lens[r] <= 256.  Replaces nothing in the reference (its
  * scorer is stateless, bb/model.py:78-87); it is the batched scorer's kernel. */
 int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void* v_cache, int64_t row_stride,
                      int64_t pos_stride, const int32_t* idx, const int32_t* lens, const void* k_new,

@@ -20,11 +20,12 @@ namespace vs {
 namespace {
 
 constexpr int DH = 64;
-constexpr int MAXL = 512;  // positions per row (scores kept in registers, 16 per lane)
+constexpr int MAXL = 256;  // positions per row (scores kept in registers, 8 per lane)
+constexpr int HPC = 4;     // heads (warps) per CTA
 
 __device__ __forceinline__ float2 bf2(uint32_t w) { return make_float2(bf16lo(w), bf16hi(w)); }
 
-__global__ void __launch_bounds__(512) row_attention_kernel(
+__global__ void __launch_bounds__(HPC * 32, 6) row_attention_kernel(
     const __nv_bfloat16* __restrict__ q, int64_t q_ld, __nv_bfloat16* __restrict__ kc,
     __nv_bfloat16* __restrict__ vc, int64_t row_stride, int64_t pos_stride, const int* __restrict__ idx,
     const int* __restrict__ lens, const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
@@ -34,7 +35,8 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
   const int r = blockIdx.x;
   const int R = d_R ? *d_R : R_host;
   if (r >= R) return;
-  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y * HPC + hw;
   if (h >= H) return;
   const int L = lens[r];
   const int64_t row = idx[r];
@@ -63,6 +65,11 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
   float mx = -INFINITY;
 #pragma unroll
   for (int i = 0; i < MAXL / 32; ++i) {
+    sc[i] = -INFINITY;
+  }
+#pragma unroll
+  for (int i = 0; i < MAXL / 32; ++i) {
+    if (32 * i >= L) break;  // warp-uniform
     const int t = lane + 32 * i;
     float s = -INFINITY;
     if (t < L) {
@@ -91,6 +98,7 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXL / 32; ++i) {
+    if (32 * i >= L) break;
     const float p = (lane + 32 * i < L) ? __expf(sc[i] - mx) : 0.f;
     sc[i] = p;
     sum += p;
@@ -102,10 +110,12 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
   // lanes: group g takes positions t = g (mod 4), lane `sub` of the group owns
   // dims 8*sub..8*sub+7 (one 16-byte V load per position); 16 positions (4 per
   // group) are loaded per iteration, groups are summed by shuffles at the end.
-  __shared__ float sp[16][MAXL];
+  __shared__ float sp[HPC][MAXL];
 #pragma unroll
-  for (int i = 0; i < MAXL / 32; ++i)
-    if (32 * i < L) sp[h][lane + 32 * i] = sc[i] * inv;
+  for (int i = 0; i < MAXL / 32; ++i) {
+    if (32 * i >= L) break;
+    sp[hw][lane + 32 * i] = sc[i] * inv;
+  }
   __syncwarp();
   const int g = lane >> 3, sub = lane & 7;
   float acc[8];
@@ -124,7 +134,7 @@ __global__ void __launch_bounds__(512) row_attention_kernel(
       if (t < L) {
         const __nv_bfloat16* vp = (has_new && t == L - 1) ? vlast : vbase + (int64_t)t * pos_stride;
         vv[u] = *reinterpret_cast<const uint4*>(vp);
-        pp[u] = sp[h][t];
+        pp[u] = sp[hw][t];
       }
     }
 #pragma unroll
@@ -163,11 +173,11 @@ extern "C" int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void
                                 const void* v_new, int64_t new_ld, void* out, int64_t out_ld, int32_t heads,
                                 int32_t head_dim, float scale, int32_t R_host, const int32_t* d_R, int32_t R_grid,
                                 void* stream) {
-  if (!q || !k_cache || !v_cache || !idx || !lens || !out || head_dim != vs::DH || heads < 1 || heads > 16 ||
+  if (!q || !k_cache || !v_cache || !idx || !lens || !out || head_dim != vs::DH || heads < 1 || heads % vs::HPC ||
       R_grid < 0 || ((k_new == nullptr) != (v_new == nullptr)))
     return VS_ERR_CONFIG;
   if (R_grid == 0) return VS_OK;
-  vs::vs_launch(vs::row_attention_kernel, dim3(R_grid), dim3(32 * heads), 0, static_cast<cudaStream_t>(stream), 
+  vs::vs_launch(vs::row_attention_kernel, dim3(R_grid, heads / vs::HPC), dim3(32 * vs::HPC), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const __nv_bfloat16*>(q), q_ld, static_cast<__nv_bfloat16*>(k_cache),
       static_cast<__nv_bfloat16*>(v_cache), row_stride, pos_stride, idx, lens,
       static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new), new_ld,

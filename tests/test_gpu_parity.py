@@ -406,7 +406,7 @@ def _graphed_decoder_run(use_graphs=True, fused_head=False):
     vocab = P.Vocabulary(500, 0, 2)
     cfg = P.DecodeConfig(k=6, n=8, epsilon=1 / 4, delta=2.0, max_candidates=3, max_len=24)
     corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(5, 40, 500, mean_len=7.0, clip=30))
-    dec = GraphedTransformerScorer(vocab, d=128, heads=2, layers=2, enc_layers=1, ffn=256, max_src=32,
+    dec = GraphedTransformerScorer(vocab, d=256, heads=4, layers=2, enc_layers=1, ffn=512, max_src=32,
                                    seed=4, tau=3.0, eos_bias=4.0, use_graphs=use_graphs, fused_head=fused_head)
     rec = LseRecorder(dec, record_logits=True)
     ev = []
