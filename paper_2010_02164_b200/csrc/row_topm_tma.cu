@@ -21,13 +21,13 @@
 //    row's (m, s) is the in-order left fold over segments 0..nseg-1, whether
 //    one warp owns the row or its segments are spread over several warps (the
 //    fold then runs in the row's finisher from per-segment pairs).
-//  * Top-M candidates use the warp-uniform threshold key θ of row_topm.cu
-//    (bootstrapped from the 32 lane maxima of a piece's first segment, raised
-//    by warp_select flushes); a segment whose m_seg < θ is skipped by one
-//    uniform branch.  Row pieces owned by several warps publish their top-M
-//    logit keys + θ; the last piece to arrive (per-row counter) merges,
-//    re-keys by logp = fp32(x - lse), selects, runs the tie-aware proof and,
-//    if unprovable, the exact radix select over the row (counted).
+//  * Top-M candidates live in a register-resident sorted list (lane j holds
+//    the j-th key) whose M-th key is the warp-uniform threshold θ (bootstrapped
+//    from the 32 lane maxima of a piece's first segment); a segment whose
+//    maximum is below θ costs one uniform compare.  Row pieces owned by
+//    several warps publish their top-M logit keys + θ; the last piece to arrive
+//    (per-row counter) merges, re-keys by logp = fp32(x - lse), selects, runs
+//    the tie-aware proof and, if unprovable, the exact radix select (counted).
 //
 // Requirements (else the caller uses row_topm.cu): 16-byte aligned rows
 // (logits and ld*sizeof(T)), V*sizeof(T) >= 4096, M <= 32.

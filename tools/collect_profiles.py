@@ -17,7 +17,7 @@ src = ROOT / "gpurun_out"
 dst = ROOT / "profiles" / rnd
 dst.mkdir(parents=True, exist_ok=True)
 summary = {}
-for rep in ("k1_fullwidth", "k1_decode", "step_kernels", "k1t_fw", "k1t_573"):
+for rep in ("k1_fullwidth", "k1_decode", "step_kernels", "k1t_fw", "k1t_573", "k5_1300"):
     p = src / f"{rep}.ncu-rep"
     if not p.exists():
         continue
@@ -48,8 +48,9 @@ if False:
     out = subprocess.run([sys.executable, str(ROOT / "tools" / "launch_summary.py"), str(src / "launches_decode.csv")],
                          capture_output=True, text=True).stdout
     (dst / "launches_decode_summary.txt").write_text(out)
-if (src / "bench.json").exists():
-    shutil.copy(src / "bench.json", dst / "bench.json")
+for name in ("bench.json", "bench_ref.json", "pytest_gpu.log", "smoke.log"):
+    if (src / name).exists():
+        shutil.copy(src / name, dst / name)
 (dst / "summary.json").write_text(json.dumps(summary, indent=1))
 # K1 DRAM traffic per launch (full-width capture: R=6400 x 42024 bf16)
 fw = summary.get("k1_fullwidth")
