@@ -388,7 +388,10 @@ def run_ours(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = len(corpus) / float(te.item())
     h2d = int(tok.nbytes + off.nbytes)
-    d2h = int(len(local_corpus) * 4 + len(local_corpus) * w["k"] * (4 + 8 + 4 * w["max_len"]))
+    # bytes of the last call's output D2H (compacted on device: counts, lengths,
+    # scores, emitted tokens packed back to back)
+    d2h = int(getattr(outs, "d2h_bytes", 0)) if world == 1 else int(
+        len(local_corpus) * 4 + len(local_corpus) * w["k"] * (4 + 8 + 4 * w["max_len"]))
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "seq/s", "n_gpus": world,

@@ -55,11 +55,13 @@ def refill_threshold(config: DecodeConfig) -> int:
 
 class DecodeResults(Sequence):
     """Per-input emitted candidates, in input order (bb/scheduler.py:287),
-    built lazily from the device output buffers copied back to the host."""
+    built lazily from the device outputs copied back to the host: per-input
+    counts, per-candidate lengths and scores, and the emitted tokens packed
+    back to back (``tok_off[o]`` = start of candidate slot ``o``)."""
 
-    def __init__(self, count, lens, scores, toks, k: int, max_len: int):
+    def __init__(self, count, lens, scores, toks, k: int, max_len: int, tok_off=None):
         self.count, self.lens, self.scores, self.toks = count, lens, scores, toks
-        self.k, self.max_len = k, max_len
+        self.k, self.max_len, self.tok_off = k, max_len, tok_off
 
     def __len__(self) -> int:
         return int(self.count.shape[0])
@@ -73,9 +75,17 @@ class DecodeResults(Sequence):
         for e in range(int(self.count[i])):
             o = i * self.k + e
             n = int(self.lens[o])
-            out.append(Candidate(tuple(int(t) for t in self.toks[o, :n]), float(self.scores[o]),
-                                 True, i))
+            if self.tok_off is None:
+                toks = self.toks[o, :n]
+            else:
+                b = int(self.tok_off[o])
+                toks = self.toks[b:b + n]
+            out.append(Candidate(tuple(int(t) for t in toks), float(self.scores[o]), True, i))
         return out
+
+    @property
+    def d2h_bytes(self) -> int:
+        return int(self.count.nbytes + self.lens.nbytes + self.scores.nbytes + self.toks.nbytes)
 
 
 class SearchEngine:
@@ -133,6 +143,7 @@ class SearchEngine:
                 setattr(self.state, f, self.t[f].data_ptr())
         self.N = 0
         self._k1_ws = None
+        self._pinned = {}  # reusable pinned D2H buffers (results)
 
     # ------------------------------------------------------------------ data
     @property
@@ -170,16 +181,35 @@ class SearchEngine:
             setattr(self.state, f, self.t[f].data_ptr())
 
     def results(self) -> DecodeResults:
-        """D2H of the output buffers (pinned) -> lazily materialised candidates."""
+        """Compact the emitted candidates on the device (counts, lengths,
+        scores, tokens packed back to back), then one D2H into reusable pinned
+        buffers: the bytes moved are those of the emitted outputs, not of the
+        [N, k, max_len] token buffer."""
         k, L, n_in = self.k, self.max_len, self.N
-        host = {f: torch.empty(self.t[f].shape, dtype=self.t[f].dtype, pin_memory=True)
-                for f in ("out_count", "out_len", "out_score", "out_tok")}
-        for f, h in host.items():
-            h.copy_(self.t[f], non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        return DecodeResults(host["out_count"].numpy(), host["out_len"].numpy(),
-                             host["out_score"].numpy(), host["out_tok"].numpy().reshape(n_in * k, L),
-                             k, L)
+        t, dev = self.t, self.device
+        count = t["out_count"][:n_in]
+        emitted = (torch.arange(k, device=dev)[None, :] < count[:, None]).reshape(-1)
+        lens = torch.where(emitted, t["out_len"][: n_in * k].clamp(0, L), 0)  # slots never written stay harmless
+        total = int(lens.sum().item())
+        slot = torch.repeat_interleave(torch.arange(n_in * k, device=dev), lens.long(), output_size=total)
+        starts = torch.cumsum(lens, 0, dtype=torch.int64) - lens
+        pos = torch.arange(total, device=dev) - starts[slot]
+        packed = t["out_tok"].view(n_in * k, L)[slot, pos]
+        src = {"count": count, "lens": lens, "score": t["out_score"][: n_in * k], "tok": packed}
+        host = {}
+        for f, d in src.items():
+            buf = self._pinned.get(f)
+            if buf is None or buf.numel() < d.numel() or buf.dtype != d.dtype:
+                buf = torch.empty(max(d.numel(), 1), dtype=d.dtype, pin_memory=True)
+                self._pinned[f] = buf
+            host[f] = buf[: d.numel()]
+            host[f].copy_(d, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        lens_h = host["lens"].numpy()
+        off = np.zeros(lens_h.shape[0], dtype=np.int64)
+        np.cumsum(lens_h[:-1], out=off[1:])
+        return DecodeResults(host["count"].numpy(), lens_h, host["score"].numpy(), host["tok"].numpy(), k, L,
+                             tok_off=off)
 
     # --------------------------------------------------------------- kernels
     def schedule(self, *, first: bool, remove: bool, admit: int, select: int) -> None:
