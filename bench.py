@@ -281,6 +281,46 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False):
 DEC_TAU, DEC_EOS_BIAS = 6.0, 20.0
 
 
+def _dec_cpu_worker(args):
+    """Spawned process: the oracle port of the reference search
+    (bb/scheduler.py run_varstream) scoring with the reference's stateless
+    protocol on the CPU — the same random-init transformer weights, fp32,
+    whole-prefix recompute per candidate (oracle/scorers.py:TorchDecoderCPU)."""
+    w, inputs = args
+    import torch
+
+    torch.set_num_threads(1)
+    from oracle import varstream_oracle as O
+    from oracle.scorers import TorchDecoderCPU
+
+    sc = TorchDecoderCPU(w["V"], w["sos"], w["eos"], seed=0, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS)
+    cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                    max_len=w["max_len"])
+    t0 = time.perf_counter()
+    _, rep = O.run_varstream(inputs, sc, cfg)
+    return time.perf_counter() - t0, rep.candidate_expansions
+
+
+def decoder_cpu_baseline(w, procs: int = 8):
+    """The reference search + CPU transformer scorer on host cores: `procs`
+    single-threaded processes, one input each, evenly strided over the
+    length-sorted corpus; seq/s = inputs / slowest process."""
+    import multiprocessing as mp
+
+    corpus = _corpus(w)
+    procs = max(1, min(procs, os.cpu_count() or 1))
+    stride = max(1, len(corpus) // procs)
+    sample = corpus[stride // 2::stride][:procs]
+    with mp.get_context("spawn").Pool(len(sample)) as pool:
+        res = pool.map(_dec_cpu_worker, [(w, [x]) for x in sample])
+    busy = max(r[0] for r in res)
+    exp = sum(r[1] for r in res)
+    return {"value": round(len(sample) / busy, 4), "unit": "seq/s", "cores": len(sample), "kind": "port",
+            "sample": f"{len(sample)} inputs (every {stride}th of the length-sorted corpus, lengths "
+                      f"{sorted(len(x) for x in sample)}), {len(sample)} processes x 1 thread, {exp} "
+                      f"candidate expansions (whole-prefix recompute per candidate, fp32), slowest {busy:.1f}s"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -430,6 +470,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and args.decoder_inputs > 0:
         line["decoder_wmt19"] = decoder_leg(w, args.decoder_inputs)
         line["decoder_wmt19_k5"] = decoder_leg(w, args.decoder_inputs, fused_head=True)
+        if args.decoder_cpu_baseline:  # ~3.5 min of host time: opt-in
+            line["decoder_wmt19"]["cpu_baseline"] = decoder_cpu_baseline(w)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
@@ -479,6 +521,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-per-proc", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decoder-cpu-baseline", action="store_true",
+                    help="also time the reference search + CPU transformer scorer (8 inputs, ~3.5 min)")
     ap.add_argument("--decoder-inputs", type=int, default=2000,
                     help="inputs for the transformer-big decoder leg (0 = skip)")
     args = ap.parse_args()

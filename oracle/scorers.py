@@ -232,3 +232,85 @@ class RecordedRowsScorer:
         key = (enc.input_id, tuple(cand.tokens))
         x = np.asarray(self.logits[key], dtype=np.float32)
         return (x - np.float32(self.lse[key])).astype(np.float32).astype(np.float64)
+
+
+class TorchDecoderCPU:
+    """Reference-protocol scorer (bb/model.py:78-87: ``encode``, stateless
+    ``score_next``) for the WMT'19-shape decoder leg's CPU baseline: the
+    random-init transformer of paper_2010_02164_b200/decoder.py rebuilt on the
+    CPU from the same seeded generator sequence (identical bf16 weights, fp32
+    compute), recomputing the whole prefix for every candidate as the
+    reference's stateless scorer protocol does.  Rows are the fp64
+    log-softmax of the logits (bb/model.py:216-217).  TEST/BASELINE
+    INFRASTRUCTURE: only bench.py's cpu-baseline legs use it."""
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, *, d: int = 1024, heads: int = 16,
+                 layers: int = 6, enc_layers: int = 6, ffn: int = 4096, seed: int = 0, tau: float = 6.0,
+                 eos_bias: float = 20.0):
+        import torch
+
+        self.torch = torch
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self.d, self.h, self.tau, self.eos_bias = d, heads, tau, eos_bias
+        g = torch.Generator(device="cpu").manual_seed(seed)
+
+        def w(*shape, std=None):  # same draw order / scaling as decoder.TransformerScorer
+            std = std if std is not None else 1.0 / math.sqrt(shape[-1])
+            return (torch.randn(*shape, generator=g) * std).to(torch.bfloat16).float()
+
+        V = vocab_size
+        self.emb = w(V, d, std=1.0)
+        self.pos = w(512, d, std=0.5)
+        self.enc = [dict(qkv=w(3 * d, d), o=w(d, d), f1=w(ffn, d), f2=w(d, ffn)) for _ in range(enc_layers)]
+        self.dec = [dict(qkv=w(3 * d, d), o=w(d, d), cq=w(d, d), ckv=w(2 * d, d), co=w(d, d),
+                         f1=w(ffn, d), f2=w(d, ffn)) for _ in range(layers)]
+        out = (torch.randn(V, d, generator=g) * (1.0 / math.sqrt(d))).to(torch.bfloat16)
+        self.out_s = (out.float() * tau).to(torch.bfloat16).float()  # tau folded, as on the device
+
+    def _attn(self, q, k, v, mask):
+        F = self.torch.nn.functional
+        dh = self.d // self.h
+
+        def split(x):
+            B, T, _ = x.shape
+            return x.view(B, T, self.h, dh).transpose(1, 2)
+
+        s = (split(q) @ split(k).transpose(-1, -2)) / math.sqrt(dh)
+        if mask is not None:
+            s = s.masked_fill(~mask, float("-inf"))
+        a = F.softmax(s, dim=-1) @ split(v)
+        B, h, T, _ = a.shape
+        return a.transpose(1, 2).reshape(B, T, h * dh)
+
+    def encode(self, tokens, input_id: int = 0) -> Encoding:
+        torch, F = self.torch, self.torch.nn.functional
+        toks = _check_input_tokens(tokens, self.vocab_size)
+        with torch.no_grad():
+            x = (self.emb[list(toks)] + self.pos[: len(toks)])[None]
+            for L in self.enc:
+                q, k, v = (x @ L["qkv"].T).split(self.d, dim=-1)
+                x = F.layer_norm(x + self._attn(q, k, v, None) @ L["o"].T, (self.d,))
+                x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (self.d,))
+            cross = [(x @ L["ckv"].T).split(self.d, dim=-1) for L in self.dec]
+        enc = Encoding(input_id, toks, len(toks))
+        self._cross = getattr(self, "_cross", {})
+        self._cross[(input_id, toks)] = cross
+        return enc
+
+    def score_next(self, enc: Encoding, cand):
+        torch, F = self.torch, self.torch.nn.functional
+        cross = self._cross[(enc.input_id, enc.tokens)]
+        prefix = list(cand.tokens)
+        T = len(prefix)
+        with torch.no_grad():
+            x = (self.emb[prefix] + self.pos[:T])[None]
+            causal = torch.ones(T, T, dtype=torch.bool).tril()[None, None]
+            for L, (ck, cv) in zip(self.dec, cross):
+                q, k, v = (x @ L["qkv"].T).split(self.d, dim=-1)
+                x = F.layer_norm(x + self._attn(q, k, v, causal) @ L["o"].T, (self.d,))
+                x = F.layer_norm(x + self._attn(x @ L["cq"].T, ck, cv, None) @ L["co"].T, (self.d,))
+                x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (self.d,))
+            lg = (x[0, -1] @ self.out_s.T).double()
+        lg[self.eos] += self.eos_bias * T / enc.input_len
+        peak = float(lg.max())
+        return (lg - (peak + math.log(float(torch.exp(lg - peak).sum())))).numpy()
