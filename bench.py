@@ -327,7 +327,7 @@ def run_ours(args):
 
     from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
     from paper_2010_02164_b200 import _native as N
-    from paper_2010_02164_b200.engine import SearchEngine
+    from paper_2010_02164_b200.engine import SearchEngine, drive_concurrent
     from paper_2010_02164_b200.harness import flatten, shard
     from paper_2010_02164_b200.scorers import DeviceHashScorer
 
@@ -356,10 +356,38 @@ def run_ours(args):
 
     from paper_2010_02164_b200.parallel import gather_results, pack_results, run_varstream_sharded
 
+    # concurrent refilling batches on this GPU (each of n slots; the rank's
+    # length-sorted shard is dealt snake-wise over them, as across GPUs)
+    S = max(1, args.streams) if world == 1 else 1
+    sub_ids = [shard(len(local_corpus), S, q) for q in range(S)]
+    engs = [eng] + [SearchEngine(cfg, vocab) for _ in range(S - 1)]
+    scs = [scorer] + [scorer.fork() for _ in range(S - 1)]
+    subs = []
+    for q in range(S):
+        st_, of_ = flatten([local_corpus[int(i)] for i in sub_ids[q]])
+        subs.append((torch.from_numpy(st_).cuda(), torch.from_numpy(of_).cuda()))
+    streams_ = [torch.cuda.Stream() for _ in range(S)]
+
     def decode(k1=None):
-        _, rep = eng.run_async(None, scorer, admit_mode=N.VS_ADMIT_VARSTREAM,
-                               select_mode=N.VS_SELECT_MIN_LT, src_tok=d_tok, src_off=d_off,
-                               materialize=False, k1_events=k1)
+        if k1 is not None or S == 1:
+            _, rep = eng.run_async(None, scorer, admit_mode=N.VS_ADMIT_VARSTREAM,
+                                   select_mode=N.VS_SELECT_MIN_LT, src_tok=d_tok, src_off=d_off,
+                                   materialize=False, k1_events=k1)
+        else:
+            cur = torch.cuda.current_stream()
+            jobs = []
+            for q in range(S):
+                streams_[q].wait_stream(cur)
+                jobs.append((streams_[q], engs[q].async_steps(None, scs[q], admit_mode=N.VS_ADMIT_VARSTREAM,
+                                                                select_mode=N.VS_SELECT_MIN_LT,
+                                                                src_tok=subs[q][0], src_off=subs[q][1])))
+            reps_ = drive_concurrent(jobs)
+            for q in range(S):
+                cur.wait_stream(streams_[q])
+            rep = reps_[0]
+            for r_ in reps_[1:]:
+                rep.timesteps += r_.timesteps
+                rep.candidate_expansions += r_.candidate_expansions
         if world > 1:  # the only collective: one ragged output gather to rank 0
             packed = pack_results(eng.t["out_count"], eng.t["out_len"], eng.t["out_score"],
                                   eng.t["out_tok"], eng.k, eng.max_len)
@@ -381,7 +409,7 @@ def run_ours(args):
         e0.record()
         for _ in range(args.steps):  # no per-kernel events inside: they would break the PDL chain
             reps.append(decode())
-            launches += 5 * eng.launched_steps + 1
+            launches += sum(5 * e.launched_steps + 1 for e in (engs if S > 1 else [eng]))
         e1.record()
         barrier()
     t_local = e0.elapsed_time(e1) / 1e3
@@ -418,7 +446,7 @@ def run_ours(args):
         if world > 1:
             outs, _ = run_varstream_sharded(corpus, scorer, cfg)
         else:
-            outs, _ = run_varstream(local_corpus, scorer, cfg)  # DecodeResults = D2H copies
+            outs, _ = run_varstream(local_corpus, scorer, cfg, streams=max(1, args.streams))
         torch.cuda.synchronize()
         if i:
             e2e_t.append(time.perf_counter() - s0)
@@ -444,6 +472,7 @@ def run_ours(args):
                    "scorer": f"device hash scorer (log-like logits, scale {w['scale']}, eos_bias "
                              f"{w['eos_bias']}) standing in for the decoder vocab projection",
                    "global_batch": len(corpus), "batch_slots_n": w["n"], "parallelism": f"shard{world}",
+                   "concurrent_batches_per_gpu": max(1, args.streams),
                    "l2": "not flushed inside the decode (producer->K1 reuse is part of the pipeline); "
                          "roofline_full_width flushes L2 and uses 538 MB > L2",
                    "timesteps_per_decode": rep.timesteps,
@@ -521,6 +550,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-per-proc", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="concurrent refilling batches (n slots each) per GPU, on separate CUDA streams")
     ap.add_argument("--decoder-cpu-baseline", action="store_true",
                     help="also time the reference search + CPU transformer scorer (8 inputs, ~3.5 min)")
     ap.add_argument("--decoder-inputs", type=int, default=2000,

@@ -316,12 +316,13 @@ class SearchEngine:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
         return self.results(), report
 
-    def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
-                  ring: int = 8, trace: bool = False, src_tok=None, src_off=None,
-                  materialize: bool = True, k1_events: list | None = None):
-        """Host-sync-free driver (no flush / no StepEvents): every kernel reads
-        R_t from device memory, status headers are streamed into a pinned ring
-        and consumed `ring` steps behind the device."""
+    def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 8,
+                    trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None):
+        """Generator form of the host-sync-free driver: every ``next()``
+        launches one step (on the CUDA stream current at that call) and
+        consumes the status snapshot ``ring`` steps behind; it returns the
+        MetricsReport (StopIteration.value).  Several engines' generators can
+        be interleaved on separate streams (``drive_concurrent``)."""
         cfgd = self.config
         self.load_corpus(corpus, src_tok=src_tok, src_off=src_off)
         scorer.bind(self)
@@ -329,13 +330,11 @@ class SearchEngine:
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
         hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
         events = [torch.cuda.Event() for _ in range(ring)]
-        stream = torch.cuda.current_stream(self.device)
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)
         launched = processed = 0
-        done = False
         self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode)
-        while not done:
+        while True:
             slot = launched % ring
             if launched - processed >= ring:  # consume the oldest snapshot
                 events[processed % ring].synchronize()
@@ -343,10 +342,10 @@ class SearchEngine:
                 if st[N.ST_ERROR]:
                     self.read_status()
                 if st[N.ST_NLIVE] == 0:
-                    done = True
                     break
                 report.record_step(int(st[N.ST_R]), int(st[N.ST_L]), cost)
                 processed += 1
+            stream = torch.cuda.current_stream(self.device)
             hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
             events[slot].record(stream)
             scorer.on_admit(self, None)
@@ -363,8 +362,45 @@ class SearchEngine:
             scorer.after_step(self, None)
             self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
             launched += 1
+            yield
         self.launched_steps = launched
         st = self.read_status()
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
+        return report
+
+    def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
+                  ring: int = 8, trace: bool = False, src_tok=None, src_off=None,
+                  materialize: bool = True, k1_events: list | None = None):
+        """Host-sync-free driver (no flush / no StepEvents): every kernel reads
+        R_t from device memory, status headers are streamed into a pinned ring
+        and consumed `ring` steps behind the device."""
+        gen = self.async_steps(corpus, scorer, admit_mode=admit_mode, select_mode=select_mode, ring=ring,
+                               trace=trace, src_tok=src_tok, src_off=src_off, k1_events=k1_events)
+        while True:
+            try:
+                next(gen)
+            except StopIteration as stop:
+                report = stop.value
+                break
         return (self.results() if materialize else None), report
+
+
+def drive_concurrent(jobs):
+    """Interleave several engines' sync-free drivers, each on its own CUDA
+    stream, one step per engine per round: independent refilling batches share
+    the GPU, so one batch's latency-bound kernels (beam step, scheduler, small
+    steps) overlap another's streaming ones.  ``jobs`` = [(stream, generator)];
+    returns the MetricsReports in job order."""
+    reports = [None] * len(jobs)
+    live = list(range(len(jobs)))
+    while live:
+        for j in list(live):
+            stream, gen = jobs[j]
+            with torch.cuda.stream(stream):
+                try:
+                    next(gen)
+                except StopIteration as stop:
+                    reports[j] = stop.value
+                    live.remove(j)
+    return reports

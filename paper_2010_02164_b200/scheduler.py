@@ -11,12 +11,16 @@ be a BatchedScorer (device) or any reference-protocol Scorer
 from __future__ import annotations
 
 import math
+from collections.abc import Sequence
+
+import torch
 
 from . import _native as N
-from .core import DecodeConfig, Vocabulary
-from .metrics import CostParams, MetricsReport
-from .engine import SearchEngine
+from .core import Candidate, DecodeConfig, Vocabulary
+from .engine import SearchEngine, drive_concurrent
 from .errors import ConfigError
+from .harness import shard
+from .metrics import CostParams, MetricsReport
 from .scorers import HostScorerAdapter
 
 ENGINES = ("greedy", "fixed", "varbeam", "varstream", "varfifo", "fixedstream")
@@ -34,10 +38,68 @@ def _vocab(scorer) -> Vocabulary:
     return v if isinstance(v, Vocabulary) else Vocabulary(v.size, v.sos, v.eos)
 
 
-def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast):
+class ConcurrentResults(Sequence):
+    """Global input order over the per-batch results of a concurrent run."""
+
+    def __init__(self, n: int, shards, parts):
+        self.where = [None] * n
+        for q, ids in enumerate(shards):
+            for li, g in enumerate(ids):
+                self.where[int(g)] = (q, li)
+        self.parts = parts
+
+    def __len__(self) -> int:
+        return len(self.where)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        q, li = self.where[i]
+        return [Candidate(c.tokens, c.score, c.finalized, i) for c in self.parts[q][li]]
+
+    @property
+    def d2h_bytes(self) -> int:
+        return sum(p.d2h_bytes for p in self.parts)
+
+
+def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
+    """`streams` independent refilling batches (each of config.n slots), the
+    length-sorted corpus dealt snake-wise over them as across GPUs, driven
+    concurrently on separate CUDA streams of one device.  Every input's output
+    is independent of batch composition (bb SPEC.md:379), so the candidates
+    equal a single-batch run's; the MetricsReport sums the batches' counters."""
+    scorers = [scorer] + [scorer.fork() for _ in range(streams - 1)]
+    shards = [shard(len(corpus), streams, q) for q in range(streams)]
+    engines, jobs = [], []
+    for q in range(streams):
+        eng = SearchEngine(config, _vocab(scorers[q]))
+        sub = [corpus[int(i)] for i in shards[q]]
+        gen = eng.async_steps(sub, scorers[q], admit_mode=admit, select_mode=select, trace=trace)
+        engines.append(eng)
+        jobs.append((torch.cuda.Stream(eng.device), gen))
+    reports = drive_concurrent(jobs)
+    parts = []
+    for eng, (stream, _) in zip(engines, jobs):
+        with torch.cuda.stream(stream):
+            parts.append(eng.results())
+    merged = MetricsReport.new(trace=trace)
+    for rep in reports:
+        merged.timesteps += rep.timesteps
+        merged.candidate_expansions += rep.candidate_expansions
+        merged.simulated_cost += rep.simulated_cost
+        if trace and rep.per_step_trace:
+            merged.per_step_trace.extend(rep.per_step_trace)
+    return ConcurrentResults(len(corpus), shards, parts), merged
+
+
+def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast, streams=1):
     if not len(corpus):
         raise ConfigError("corpus must be nonempty")
     bs = _as_batched(scorer, corpus)
+    if streams > 1:
+        if on_step is not None or (flush and config.flush_interval) or not hasattr(bs, "fork"):
+            raise ConfigError("streams > 1 needs a forkable device scorer, no on_step and no flush valve")
+        return _run_concurrent(corpus, bs, config, admit, select, trace, streams)
     eng = SearchEngine(config, _vocab(bs))
     if fast and on_step is None and not (flush and config.flush_interval):
         if not isinstance(bs, HostScorerAdapter) and not getattr(bs, "host_sync", False):
@@ -47,10 +109,11 @@ def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast):
 
 
 def run_varstream(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on_step=None,
-                  fast: bool = True):
-    """ε-refill + min-l_t selection (bb/scheduler.py:314-340)."""
+                  fast: bool = True, streams: int = 1):
+    """ε-refill + min-l_t selection (bb/scheduler.py:314-340).  ``streams`` > 1
+    runs that many independent refilling batches concurrently on one GPU."""
     return _run(corpus, scorer, config, N.VS_ADMIT_VARSTREAM, N.VS_SELECT_MIN_LT, True, trace,
-                on_step, fast)
+                on_step, fast, streams)
 
 
 def run_varbeam(corpus, scorer, config: DecodeConfig, *, trace: bool = False, on_step=None,

@@ -61,6 +61,11 @@ class DeviceHashScorer:
         self.code = N.VS_DTYPE_BF16 if dtype == "bf16" else N.VS_DTYPE_F32
         self._buf = None
 
+    def fork(self) -> "DeviceHashScorer":
+        """An identical scorer for another engine (concurrent batches)."""
+        return DeviceHashScorer(self.vocab, self.seed, scale=self.scale, power=self.power,
+                                eos_bias=self.eos_bias, dtype=self.dtype)
+
     def bind(self, engine) -> None:
         V = self.vocab.size
         ld = (V + 7) // 8 * 8  # 16-byte aligned rows

@@ -493,3 +493,16 @@ def test_graphed_decoder_with_fused_k5_head_matches_oracle_replay():
         want_l = dec.full_forward(corpus[iid], toks).cpu().numpy()
         got = rec.logit_table[(iid, toks)]
         assert np.max(np.abs(got - want_l)) <= 0.06 + 0.02 * float(np.max(np.abs(want_l)))
+
+
+def test_concurrent_batches_match_single_batch():
+    """run_varstream(streams=3): three refilling batches driven concurrently on
+    separate CUDA streams produce exactly the single-batch candidates."""
+    P, N, SearchEngine, DeviceHashScorer, _, _ = _pkg()
+    vocab = P.Vocabulary(5000, 0, 2)
+    cfg = P.DecodeConfig(k=8, n=16, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=40)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(3, 300, 5000, mean_len=9.0, clip=30))
+    sc = DeviceHashScorer(vocab, 17, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    one, rep1 = P.run_varstream(corpus, sc, cfg)
+    many, rep3 = P.run_varstream(corpus, sc.fork(), cfg, streams=3)
+    assert [[(c.tokens, c.score) for c in per] for per in many] == [[(c.tokens, c.score) for c in per] for per in one]
