@@ -144,6 +144,10 @@ class SearchEngine:
         self.N = 0
         self._k1_ws = None
         self._pinned = {}  # reusable pinned D2H buffers (results)
+        self._hdr = None   # pinned status ring of the sync-free driver
+        self._bufs = {}    # grow-only corpus / output buffers
+        self._forks = {}   # scorer forks bound to this engine (concurrent batches)
+        self._graphs, self._graph_key = None, None
 
     # ------------------------------------------------------------------ data
     @property
@@ -167,18 +171,30 @@ class SearchEngine:
             raise ConfigError("corpus must be nonempty")
         self.N = n_in
         dev = self.device
-        self.t["src_off"] = src_off.to(dev, non_blocking=True)
-        self.t["src_tok"] = (src_tok if src_tok.numel() else torch.zeros(1, dtype=torch.int32)).to(
-            dev, non_blocking=True)
+        if not src_tok.numel():
+            src_tok = torch.zeros(1, dtype=torch.int32)
+        # host inputs land in grow-only device buffers, so device pointers (and
+        # the captured step graphs that hold them) stay valid across calls
+        self.t["src_off"] = src_off if src_off.is_cuda else self._grow("src_off", src_off)
+        self.t["src_tok"] = src_tok if src_tok.is_cuda else self._grow("src_tok", src_tok)
         k, L = self.k, self.max_len
-        if self.t.get("out_count") is None or self.t["out_count"].shape[0] != n_in:
-            # only entries the beam step emits are ever read; admission zeroes counts
-            self.t["out_count"] = torch.zeros(n_in, dtype=torch.int32, device=dev)
-            self.t["out_len"] = torch.empty(n_in * k, dtype=torch.int32, device=dev)
-            self.t["out_score"] = torch.empty(n_in * k, dtype=torch.float64, device=dev)
-            self.t["out_tok"] = torch.empty(n_in * k * L, dtype=torch.int32, device=dev)
+        for f, n, dt in (("out_count", n_in, torch.int32), ("out_len", n_in * k, torch.int32),
+                         ("out_score", n_in * k, torch.float64), ("out_tok", n_in * k * L, torch.int32)):
+            buf = self._bufs.get(f)
+            if buf is None or buf.numel() < n:  # only emitted entries are ever read
+                buf = self._bufs[f] = torch.empty(n, dtype=dt, device=dev)
+            self.t[f] = buf[:n]
         for f in ("src_off", "src_tok", "out_count", "out_len", "out_score", "out_tok"):
             setattr(self.state, f, self.t[f].data_ptr())
+
+    def _grow(self, name: str, src: torch.Tensor) -> torch.Tensor:
+        buf = self._bufs.get(name)
+        n = src.numel()
+        if buf is None or buf.numel() < n:
+            buf = self._bufs[name] = torch.empty(n + n // 4, dtype=src.dtype, device=self.device)
+        view = buf[:n]
+        view.copy_(src, non_blocking=True)
+        return view
 
     def results(self) -> DecodeResults:
         """Compact the emitted candidates on the device (counts, lengths,
@@ -194,7 +210,7 @@ class SearchEngine:
         slot = torch.repeat_interleave(torch.arange(n_in * k, device=dev), lens.long(), output_size=total)
         starts = torch.cumsum(lens, 0, dtype=torch.int64) - lens
         pos = torch.arange(total, device=dev) - starts[slot]
-        packed = t["out_tok"].view(n_in * k, L)[slot, pos]
+        packed = t["out_tok"][: n_in * k * L].view(n_in * k, L)[slot, pos]
         src = {"count": count, "lens": lens, "score": t["out_score"][: n_in * k], "tok": packed}
         host = {}
         for f, d in src.items():
@@ -205,11 +221,12 @@ class SearchEngine:
             host[f] = buf[: d.numel()]
             host[f].copy_(d, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
-        lens_h = host["lens"].numpy()
+        # the pinned staging buffers are reused by the next call: results own copies
+        lens_h = host["lens"].numpy().copy()
         off = np.zeros(lens_h.shape[0], dtype=np.int64)
         np.cumsum(lens_h[:-1], out=off[1:])
-        return DecodeResults(host["count"].numpy(), lens_h, host["score"].numpy(), host["tok"].numpy(), k, L,
-                             tok_off=off)
+        return DecodeResults(host["count"].numpy().copy(), lens_h, host["score"].numpy().copy(),
+                             host["tok"].numpy().copy(), k, L, tok_off=off)
 
     # --------------------------------------------------------------- kernels
     def schedule(self, *, first: bool, remove: bool, admit: int, select: int) -> None:
@@ -328,11 +345,18 @@ class SearchEngine:
         scorer.bind(self)
         report = MetricsReport.new(trace=trace)
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
-        hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
+        if self._hdr is None or self._hdr.shape[0] != ring:
+            self._hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
+        hdr = self._hdr
         events = [torch.cuda.Event() for _ in range(ring)]
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)
         launched = processed = 0
+        # one CUDA graph per ring slot replays the whole step (status snapshot,
+        # scorer, K1, K2, K3) when the scorer only launches device work
+        graphs = None
+        if getattr(scorer, "graph_safe", False) and k1_events is None:
+            graphs = self._step_graphs(scorer, ring, admit_mode, select_mode)
         self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode)
         while True:
             slot = launched % ring
@@ -346,6 +370,12 @@ class SearchEngine:
                 report.record_step(int(st[N.ST_R]), int(st[N.ST_L]), cost)
                 processed += 1
             stream = torch.cuda.current_stream(self.device)
+            if graphs is not None:
+                graphs[slot].replay()
+                events[slot].record(stream)
+                launched += 1
+                yield
+                continue
             hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
             events[slot].record(stream)
             scorer.on_admit(self, None)
@@ -368,6 +398,34 @@ class SearchEngine:
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
         return report
+
+    def _step_graphs(self, scorer, ring: int, admit_mode: int, select_mode: int):
+        """Capture (once per engine state / scorer binding) one graph per ring
+        slot: status snapshot -> pinned slot, scorer launches, K1, K2, K3."""
+        key = (id(scorer), ring, admit_mode, select_mode,
+               tuple(getattr(self.state, f) for f in N.STATE_FIELDS), self._hdr.data_ptr())
+        if self._graph_key == key:
+            return self._graphs
+        cap, d_R = self.capacity, self.status_ptr(N.ST_R)
+        nbytes = int(self.lib.vs_row_lse_topm_ws_bytes(cap, self.vocab.size, N.VS_DTYPE_F32))
+        if self._k1_ws is None or self._k1_ws.numel() < nbytes:  # allocate outside the capture
+            self._k1_ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        torch.cuda.current_stream(self.device).synchronize()
+        graphs = []
+        for slot in range(ring):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
+                scorer.on_admit(self, None)
+                logits, code = scorer.logits(self, None)
+                if code != N.VS_K1_DONE:
+                    self.row_topm(logits, code, 0, cap, d_R)
+                self.beam_step()
+                scorer.after_step(self, None)
+                self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
+            graphs.append(g)
+        self._graphs, self._graph_key = graphs, key
+        return graphs
 
     def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
                   ring: int = 8, trace: bool = False, src_tok=None, src_off=None,

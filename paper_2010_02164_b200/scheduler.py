@@ -62,21 +62,45 @@ class ConcurrentResults(Sequence):
         return sum(p.d2h_bytes for p in self.parts)
 
 
+_ENGINES: dict = {}
+
+
+def _engine(config: DecodeConfig, vocab: Vocabulary, q: int = 0):
+    """Engines (and their streams) are reused across calls with the same
+    config and vocabulary on the current device: their buffers and captured
+    step graphs persist, so a repeated call costs only the decode."""
+    key = (config, (vocab.size, vocab.sos, vocab.eos), torch.cuda.current_device(), q)
+    hit = _ENGINES.get(key)
+    if hit is None:
+        eng = SearchEngine(config, vocab)
+        hit = _ENGINES[key] = (eng, torch.cuda.Stream(eng.device) if q else None)
+    return hit
+
+
+def _fork_for(eng: SearchEngine, scorer):
+    sig = getattr(scorer, "signature", None)
+    if sig is None:
+        return scorer.fork()
+    if sig not in eng._forks:
+        eng._forks[sig] = scorer.fork()
+    return eng._forks[sig]
+
+
 def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
     """`streams` independent refilling batches (each of config.n slots), the
     length-sorted corpus dealt snake-wise over them as across GPUs, driven
     concurrently on separate CUDA streams of one device.  Every input's output
     is independent of batch composition (bb SPEC.md:379), so the candidates
     equal a single-batch run's; the MetricsReport sums the batches' counters."""
-    scorers = [scorer] + [scorer.fork() for _ in range(streams - 1)]
     shards = [shard(len(corpus), streams, q) for q in range(streams)]
     engines, jobs = [], []
     for q in range(streams):
-        eng = SearchEngine(config, _vocab(scorers[q]))
+        eng, stream = _engine(config, _vocab(scorer), q)
+        sc = scorer if q == 0 else _fork_for(eng, scorer)
         sub = [corpus[int(i)] for i in shards[q]]
-        gen = eng.async_steps(sub, scorers[q], admit_mode=admit, select_mode=select, trace=trace)
+        gen = eng.async_steps(sub, sc, admit_mode=admit, select_mode=select, trace=trace)
         engines.append(eng)
-        jobs.append((torch.cuda.Stream(eng.device), gen))
+        jobs.append((stream, gen))
     reports = drive_concurrent(jobs)
     parts = []
     for eng, (stream, _) in zip(engines, jobs):
@@ -100,10 +124,12 @@ def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast, str
         if on_step is not None or (flush and config.flush_interval) or not hasattr(bs, "fork"):
             raise ConfigError("streams > 1 needs a forkable device scorer, no on_step and no flush valve")
         return _run_concurrent(corpus, bs, config, admit, select, trace, streams)
-    eng = SearchEngine(config, _vocab(bs))
     if fast and on_step is None and not (flush and config.flush_interval):
         if not isinstance(bs, HostScorerAdapter) and not getattr(bs, "host_sync", False):
+            eng = _engine(config, _vocab(bs))[0] if getattr(bs, "graph_safe", False) else \
+                SearchEngine(config, _vocab(bs))
             return eng.run_async(corpus, bs, admit_mode=admit, select_mode=select, trace=trace)
+    eng = SearchEngine(config, _vocab(bs))
     return eng.run(corpus, bs, admit_mode=admit, select_mode=select, flush_enabled=flush,
                    trace=trace, on_step=on_step)
 

@@ -61,6 +61,12 @@ class DeviceHashScorer:
         self.code = N.VS_DTYPE_BF16 if dtype == "bf16" else N.VS_DTYPE_F32
         self._buf = None
 
+    graph_safe = True  # launches device work only: the sync-free step can be a CUDA graph
+
+    @property
+    def signature(self) -> tuple:
+        return ("hash", self.vocab.size, self.seed, self.scale, self.power, self.eos_bias, self.dtype)
+
     def fork(self) -> "DeviceHashScorer":
         """An identical scorer for another engine (concurrent batches)."""
         return DeviceHashScorer(self.vocab, self.seed, scale=self.scale, power=self.power,
