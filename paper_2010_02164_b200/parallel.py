@@ -36,6 +36,36 @@ def pack_results(count: torch.Tensor, lens: torch.Tensor, scores: torch.Tensor, 
     return count.to(torch.int32), lens_e, scores_e, flat
 
 
+def _excl_cumsum(x: torch.Tensor) -> torch.Tensor:
+    return torch.cumsum(x.long(), 0) - x.long()
+
+
+def _ragged_index(starts: torch.Tensor, lens: torch.Tensor) -> torch.Tensor:
+    """Concatenation of ranges [starts[i], starts[i] + lens[i])."""
+    total = int(lens.sum())
+    seg = torch.repeat_interleave(torch.arange(lens.numel(), device=lens.device), lens.long(), output_size=total)
+    return starts.long()[seg] + (torch.arange(total, device=lens.device) - _excl_cumsum(lens)[seg])
+
+
+def merge_packs(packs, sub_ids, n_local: int):
+    """Merge the packed outputs of concurrent batches (pack q holds the inputs
+    ``sub_ids[q]`` of this rank's shard, in that order) into one pack in the
+    shard's order — the layout gather_results expects."""
+    counts = torch.cat([p[0] for p in packs]).long()
+    lens = torch.cat([p[1] for p in packs])
+    scores = torch.cat([p[2] for p in packs])
+    toks = torch.cat([p[3] for p in packs])
+    dev = counts.device
+    order = torch.cat([torch.as_tensor(np.asarray(ids), dtype=torch.int64) for ids in sub_ids]).to(dev)
+    perm = torch.empty(n_local, dtype=torch.int64, device=dev)
+    perm[order] = torch.arange(order.numel(), device=dev)  # local input -> position in the concatenation
+    count_l = counts[perm]
+    cand = _ragged_index(_excl_cumsum(counts)[perm], count_l)
+    lens_l = lens[cand]
+    tok = _ragged_index(_excl_cumsum(lens)[cand], lens_l)
+    return count_l.to(torch.int32), lens_l.to(torch.int32), scores[cand], toks[tok].to(torch.int32)
+
+
 def _all_gather_ragged(t: torch.Tensor, group=None) -> list[torch.Tensor]:
     world = dist.get_world_size(group)
     size = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
@@ -95,7 +125,7 @@ def gather_results(packed, n_total: int, group=None, dst: int = 0):
     return ShardedResults(n_total, parts)
 
 
-def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0):
+def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0, streams: int = 1):
     """Public multi-GPU entry: this rank decodes its snake-dealt shard of the
     (length-sorted) corpus on its current CUDA device; outputs are gathered
     to rank `dst`.  Returns (ShardedResults | None, local MetricsReport)."""
@@ -108,7 +138,31 @@ def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0):
     mine = shard(len(corpus), world, rank)
     local = [corpus[i] for i in mine]
     dev = torch.device(f"cuda:{torch.cuda.current_device()}")
-    if local:
+    if local and streams > 1 and len(local) >= streams:  # concurrent batches on this GPU
+        from .engine import drive_concurrent
+        from .scheduler import _engine, _fork_for
+
+        subs = [shard(len(local), streams, q) for q in range(streams)]
+        engs, jobs = [], []
+        for q in range(streams):
+            eng, stream = _engine(config, _vocab(scorer), q)
+            sc = scorer if q == 0 else _fork_for(eng, scorer)
+            engs.append(eng)
+            jobs.append((stream, eng.async_steps([local[int(i)] for i in subs[q]], sc,
+                                                 admit_mode=N.VS_ADMIT_VARSTREAM,
+                                                 select_mode=N.VS_SELECT_MIN_LT)))
+        reps = drive_concurrent(jobs)
+        for _, st in jobs:
+            if st is not None:
+                torch.cuda.current_stream().wait_stream(st)
+        rep = reps[0]
+        for r_ in reps[1:]:
+            rep.timesteps += r_.timesteps
+            rep.candidate_expansions += r_.candidate_expansions
+            rep.simulated_cost += r_.simulated_cost
+        packed = merge_packs([pack_results(e.t["out_count"], e.t["out_len"], e.t["out_score"], e.t["out_tok"],
+                                           e.k, e.max_len) for e in engs], subs, len(local))
+    elif local:
         eng = SearchEngine(config, _vocab(scorer))
         _, rep = eng.run_async(local, scorer, admit_mode=N.VS_ADMIT_VARSTREAM,
                                select_mode=N.VS_SELECT_MIN_LT, materialize=False)

@@ -83,3 +83,35 @@ def test_snake_shard_is_a_balanced_partition(world):
     assert max(sums) / max(1, min(sums)) < 1.05
     for p in parts:  # each shard stays length-sorted
         assert np.all(np.diff(lens[p]) <= 0)
+
+
+def test_merge_packs_restores_shard_order():
+    """Concurrent batches' packed outputs merge into the shard-order pack."""
+    from paper_2010_02164_b200.harness import shard
+    from paper_2010_02164_b200.parallel import merge_packs
+
+    rng = np.random.default_rng(0)
+    n = 23
+    want = []
+    for i in range(n):
+        c = int(rng.integers(1, 4))
+        want.append([(list(rng.integers(0, 50, int(rng.integers(1, 6)))), float(rng.random())) for _ in range(c)])
+    subs = [shard(n, 3, q) for q in range(3)]
+    packs = []
+    for ids in subs:
+        cnt = torch.tensor([len(want[i]) for i in ids], dtype=torch.int32)
+        lens = torch.tensor([len(t) for i in ids for t, _ in want[i]], dtype=torch.int32)
+        sc = torch.tensor([s for i in ids for _, s in want[i]], dtype=torch.float64)
+        tk = torch.tensor([x for i in ids for t, _ in want[i] for x in t], dtype=torch.int32)
+        packs.append((cnt, lens, sc, tk))
+    cnt, lens, sc, tk = merge_packs(packs, subs, n)
+    got, e, o = [], 0, 0
+    for i in range(n):
+        per = []
+        for _ in range(int(cnt[i])):
+            L = int(lens[e])
+            per.append((tk[o:o + L].tolist(), float(sc[e])))
+            o += L
+            e += 1
+        got.append(per)
+    assert got == [[(list(map(int, t)), s) for t, s in w] for w in want]
