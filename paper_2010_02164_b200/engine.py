@@ -402,7 +402,7 @@ class SearchEngine:
     def _step_graphs(self, scorer, ring: int, admit_mode: int, select_mode: int):
         """Capture (once per engine state / scorer binding) one graph per ring
         slot: status snapshot -> pinned slot, scorer launches, K1, K2, K3."""
-        key = (id(scorer), ring, admit_mode, select_mode,
+        key = (id(scorer), ring, admit_mode, select_mode, self.N,  # N is a K3 launch argument
                tuple(getattr(self.state, f) for f in N.STATE_FIELDS), self._hdr.data_ptr())
         if self._graph_key == key:
             return self._graphs

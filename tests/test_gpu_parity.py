@@ -506,3 +506,25 @@ def test_concurrent_batches_match_single_batch():
     one, rep1 = P.run_varstream(corpus, sc, cfg)
     many, rep3 = P.run_varstream(corpus, sc.fork(), cfg, streams=3)
     assert [[(c.tokens, c.score) for c in per] for per in many] == [[(c.tokens, c.score) for c in per] for per in one]
+
+
+def test_repeated_calls_reuse_engine_and_graphs_correctly():
+    """The public API reuses engines, buffers and captured step graphs across
+    calls: corpora of different sizes (larger, smaller, same) in sequence, on
+    1 and 3 concurrent batches, each give exactly the synchronous driver's
+    candidates (that path is checked against the oracle above).  A stale graph
+    (e.g. the K3 input-count argument) would show up here."""
+    P, N, SearchEngine, DeviceHashScorer, _, LseRecorder = _pkg()
+    from oracle.scorers import HashLogitsCPU, LseReplayScorer
+
+    vocab = P.Vocabulary(3000, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=12, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=30)
+    sc = DeviceHashScorer(vocab, 23, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    for seed, n_in in [(1, 90), (2, 140), (3, 40), (4, 140)]:
+        corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(seed, n_in, 3000, mean_len=8.0, clip=25))
+        ref_out, _ = P.run_varstream(corpus, LseRecorder(sc), cfg)  # sync driver: exports lse
+        fast, _ = P.run_varstream(corpus, sc, cfg)
+        many, _ = P.run_varstream(corpus, sc, cfg, streams=3)
+        sig = [[(c.tokens, c.score) for c in per] for per in ref_out]
+        assert [[(c.tokens, c.score) for c in per] for per in fast] == sig
+        assert [[(c.tokens, c.score) for c in per] for per in many] == sig
