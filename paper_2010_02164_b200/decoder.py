@@ -241,6 +241,17 @@ class GraphedTransformerScorer(TransformerScorer):
     def _project(self, h):
         return (h @ self.out_s.T).float()
 
+    def fork(self) -> "GraphedTransformerScorer":
+        """Same weights (shared tensors), separate caches/graphs: a scorer for
+        another engine running a concurrent batch."""
+        import copy
+
+        other = copy.copy(self)
+        other._bound = None
+        other.graphs = {}
+        other.pool = None
+        return other
+
     def bind(self, engine) -> None:
         n, k, Lmax = engine.n, engine.k, engine.max_len
         if Lmax > self.pos.shape[0]:
@@ -355,7 +366,7 @@ class GraphedTransformerScorer(TransformerScorer):
             g = torch.cuda.CUDAGraph()
             if self.pool is None:
                 self.pool = torch.cuda.graph_pool_handle()
-            with torch.cuda.graph(g, pool=self.pool):
+            with torch.cuda.graph(g, pool=self.pool, capture_error_mode="thread_local"):
                 self._body(Rb)
             self.graphs[Rb] = g
         g.replay()
