@@ -355,9 +355,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs only: run every rank on one device over gloo (multi-rank path on a 1-GPU box)
+    if os.environ.get("VS_BENCH_DEVICE") is not None:
+        local = int(os.environ["VS_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("VS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     w = WORKLOADS[args.workload]
     if args.n_inputs:
         w = dict(w, N=args.n_inputs)

@@ -152,7 +152,7 @@ def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0, s
                                                  admit_mode=N.VS_ADMIT_VARSTREAM,
                                                  select_mode=N.VS_SELECT_MIN_LT)))
         reps = drive_concurrent(jobs)
-        for _, st in jobs:
+        for st, _ in jobs:
             if st is not None:
                 torch.cuda.current_stream().wait_stream(st)
         rep = reps[0]
