@@ -528,3 +528,50 @@ def test_repeated_calls_reuse_engine_and_graphs_correctly():
         sig = [[(c.tokens, c.score) for c in per] for per in ref_out]
         assert [[(c.tokens, c.score) for c in per] for per in fast] == sig
         assert [[(c.tokens, c.score) for c in per] for per in many] == sig
+
+
+def _sharded_worker(rank, world, port, out_path):
+    import os
+    import pickle
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2010_02164_b200 as P
+    from paper_2010_02164_b200.parallel import run_varstream_sharded
+    from paper_2010_02164_b200.scorers import DeviceHashScorer
+
+    vocab = P.Vocabulary(3000, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=12, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=30)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(9, 150, 3000, mean_len=8.0, clip=25))
+    sc = DeviceHashScorer(vocab, 29, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    res, _ = run_varstream_sharded(corpus, sc, cfg, streams=2)
+    if rank == 0:
+        with open(out_path, "wb") as f:
+            pickle.dump([[(c.tokens, c.score) for c in per] for per in res], f)
+    dist.destroy_process_group()
+
+
+def test_sharded_concurrent_run_gathers_single_run_outputs(tmp_path):
+    """Two ranks (gloo, sharing this GPU), each running 2 concurrent batches:
+    rank 0's gathered outputs equal a single-process, single-batch decode."""
+    import pickle
+    import socket
+
+    import torch.multiprocessing as mp
+
+    P, N, SearchEngine, DeviceHashScorer, _, _ = _pkg()
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = tmp_path / "sharded.pkl"
+    mp.spawn(_sharded_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    vocab = P.Vocabulary(3000, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=12, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=30)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(9, 150, 3000, mean_len=8.0, clip=25))
+    sc = DeviceHashScorer(vocab, 29, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    want, _ = P.run_varstream(corpus, sc, cfg)
+    got = pickle.loads(out.read_bytes())
+    assert got == [[(c.tokens, c.score) for c in per] for per in want]
