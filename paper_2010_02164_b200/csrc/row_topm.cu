@@ -243,13 +243,13 @@ __device__ __forceinline__ Cand append_fast(Cand c, float x0, float x1, float x2
 // ceil(R*W/T) * (c0 + 1/W) over W in {1,2,4,8} (T = resident warps, c0 =
 // per-task boot/epilogue cost relative to streaming a whole row) — balances
 // wave quantisation against the per-warp fixed cost.
-__host__ __device__ __forceinline__ int pick_w(int R, int V, int T) {
+__host__ __device__ __forceinline__ int pick_w(int R, int V, int T, float c0 = PICKW_C0) {
   if (V < 4096 || R <= 0) return 1;
   int best = 1;
   float bc = 1e30f;
   for (int w = 1; w <= WPC; w <<= 1) {
     const float waves = (float)(((long)R * w + T - 1) / T);
-    const float cost = waves * (PICKW_C0 + 1.0f / w);
+    const float cost = waves * (c0 + 1.0f / w);
     if (cost < bc - 1e-6f) {
       bc = cost;
       best = w;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
     int* __restrict__ fb_count, int normalized, int sms, int flush_min, int pf_batches,
-    int warps_per_sm) {
+    int warps_per_sm, float c0) {
   VS_PDL_ENTRY();
   constexpr int VEC = 16 / sizeof(T);
   __shared__ uint64_t sbuf[WPC][CAPW];
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   __shared__ PartSmem spart[WPC];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = d_R ? *d_R : R_host;
-  const int W = pick_w(R, V, sms * warps_per_sm);
+  const int W = pick_w(R, V, sms * warps_per_sm, c0);
   const int part = wid % W, leader = wid - part;
   const int r = blockIdx.x * (WPC / W) + wid / W;
   if (blockIdx.x * (WPC / W) >= R) return;  // whole CTA idle (uniform)
@@ -538,8 +538,11 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  static int variant = -1, flush_min = FLUSH_MIN, pf = 0;  // knobs: VS_K1_VARIANT/_FLUSH/_PF
+  static int variant = -1, flush_min = FLUSH_MIN, pf = 0;  // knobs: VS_K1_VARIANT/_FLUSH/_PF/_C0
+  static float c0 = PICKW_C0;
   if (variant < 0) {
+    const char* c = getenv("VS_K1_C0");
+    if (c) c0 = (float)atof(c);
     const char* q = getenv("VS_K1_PF");
     if (q) pf = atoi(q);
     const char* e = getenv("VS_K1_VARIANT");
@@ -555,20 +558,20 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     static int cached_rows = -1, cached_grid = 0, cached_T = 0;
     if (rows != cached_rows || Tw != cached_T) {
       int g = 1;
-      for (int r = 1; r <= rows; ++r) g = max(g, (r * pick_w(r, V, Tw) + WPC - 1) / WPC);
+      for (int r = 1; r <= rows; ++r) g = max(g, (r * pick_w(r, V, Tw, c0) + WPC - 1) / WPC);
       cached_rows = rows;
       cached_T = Tw;
       cached_grid = g;
     }
     grid = cached_grid;
   } else {
-    grid = (rows * pick_w(rows, V, Tw) + WPC - 1) / WPC;
+    grid = (rows * pick_w(rows, V, Tw, c0) + WPC - 1) / WPC;
   }
   const T* p = static_cast<const T*>(logits);
 #define VS_K1_LAUNCH(U_, B_)                                                                            \
   vs::vs_launch(row_lse_topm_warp_kernel<T, U_, B_>, dim3(grid), dim3(WPC * 32), 0, st, p, ld, V, M, R_host, d_R, top_tok, \
                                                                  top_logp, row_lse, fb, norm, sms, flush_min, pf, \
-                                                                 ctas_per_sm * WPC)
+                                                                 ctas_per_sm * WPC, c0)
   switch (variant) {
     case 0: VS_K1_LAUNCH(4, 2); break;
     case 3: VS_K1_LAUNCH(3, 3); break;
