@@ -520,8 +520,11 @@ def run_ours(args):
                    "concurrency": f"{S} independent refilling batches of n={w['n']} slots per GPU on separate "
                                   "CUDA streams (the corpus dealt snake-wise over them, as across GPUs); "
                                   "outputs identical to one batch (tested)",
-                   "l2": "not flushed inside the decode (producer->K1 reuse is part of the pipeline); "
-                         "roofline_full_width flushes L2 and uses 538 MB > L2",
+                   "l2": "inputs larger than L2: one bench step streams "
+                         f"{rep.candidate_expansions * w['V'] * 2 / 1e9:.1f} GB of logits through K1 "
+                         "(L2 126 MB); not flushed between the decode's own kernels (producer -> K1 "
+                         "reuse is part of the pipeline); roofline_full_width flushes L2 (256 MB write) "
+                         "before each 538 MB launch",
                    "timesteps_per_decode": rep.timesteps,
                    "expansions_per_decode": rep.candidate_expansions,
                    "expansions_per_step": round(rep.expansions_per_step, 1)},
