@@ -382,8 +382,7 @@ def run_ours(args):
     tok, off = flatten(local_corpus)
     d_tok, d_off = torch.from_numpy(tok).cuda(), torch.from_numpy(off).cuda()
 
-    from paper_2010_02164_b200.parallel import (gather_results, merge_packs, pack_results,
-                                                run_varstream_sharded)
+    from paper_2010_02164_b200.parallel import gather_packed, merge_packs, pack_results, run_varstream_sharded
 
     # concurrent refilling batches on this GPU (each of n slots; the rank's
     # length-sorted shard is dealt snake-wise over them, as across GPUs)
@@ -422,7 +421,7 @@ def run_ours(args):
             packs = [pack_results(e.t["out_count"], e.t["out_len"], e.t["out_score"], e.t["out_tok"], e.k,
                                   e.max_len) for e in used]
             packed = packs[0] if len(used) == 1 else merge_packs(packs, sub_ids, len(local_corpus))
-            gather_results(packed, len(corpus))
+            gather_packed(packed)  # device-resident; the e2e leg builds the host-side results
         return rep
 
     def barrier():

@@ -81,21 +81,27 @@ def _all_gather_ragged(t: torch.Tensor, group=None) -> list[torch.Tensor]:
 
 
 class ShardedResults(Sequence):
-    """Global-order per-input candidate lists assembled on the gathering rank."""
+    """Global-order per-input candidate lists assembled on the gathering rank
+    (index arrays built with numpy: no per-input Python work up front)."""
 
     def __init__(self, n_total: int, parts):
         self.n = n_total
-        self.index = [None] * n_total  # input -> (part, first candidate, count)
+        self.part = np.full(n_total, -1, dtype=np.int32)      # input -> part
+        self.cfirst = np.zeros(n_total, dtype=np.int64)       # input -> first candidate in its part
+        self.ccount = np.zeros(n_total, dtype=np.int64)
         self.parts = []
         for gids, count, lens, scores, toks in parts:
+            gids = np.asarray(gids, dtype=np.int64)
+            count = np.asarray(count, dtype=np.int64)
             offs = np.zeros(len(lens) + 1, dtype=np.int64)
             np.cumsum(lens, out=offs[1:])
             cstart = np.zeros(len(count) + 1, dtype=np.int64)
             np.cumsum(count, out=cstart[1:])
             p = len(self.parts)
             self.parts.append((lens, scores, toks, offs))
-            for li, g in enumerate(gids):
-                self.index[int(g)] = (p, int(cstart[li]), int(count[li]))
+            self.part[gids] = p
+            self.cfirst[gids] = cstart[:-1]
+            self.ccount[gids] = count
 
     def __len__(self) -> int:
         return self.n
@@ -103,10 +109,16 @@ class ShardedResults(Sequence):
     def __getitem__(self, i):
         if isinstance(i, slice):
             return [self[j] for j in range(*i.indices(self.n))]
-        p, c0, cnt = self.index[i]
+        p, c0, cnt = int(self.part[i]), int(self.cfirst[i]), int(self.ccount[i])
         lens, scores, toks, offs = self.parts[p]
         return [Candidate(tuple(int(t) for t in toks[offs[c]:offs[c + 1]]), float(scores[c]), True, i)
                 for c in range(c0, c0 + cnt)]
+
+
+def gather_packed(packed, group=None):
+    """The one collective: all-gather every rank's packed (ragged) results;
+    returns, per field, the list of every rank's tensor (device-resident)."""
+    return [_all_gather_ragged(t, group) for t in packed]
 
 
 def gather_results(packed, n_total: int, group=None, dst: int = 0):
@@ -114,7 +126,7 @@ def gather_results(packed, n_total: int, group=None, dst: int = 0):
     ShardedResults in global input order, the others return None."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    gathered = [_all_gather_ragged(t, group) for t in packed]
+    gathered = gather_packed(packed, group)
     if rank != dst:
         return None
     parts = []
