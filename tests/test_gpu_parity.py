@@ -287,6 +287,12 @@ HASH_CASES = [
     ("wmt_like", 42024, 50, 16, 5, 1.5, 40, 1 / 6, 24, "bf16", 0.5, 0, 7.5),
     ("immediate", 1000, 5, 16, 5, 1.5, 32, 1 / 6, 96, "bf16", 0.5, 0, 4.0, "immediate"),
     ("immediate_k16", 2048, 16, 8, 16, 3.0, 24, 1 / 4, 40, "f32", 0.5, 0, 4.0, "immediate"),
+    # edge shapes: one slot x width one; the length cap draining every beam;
+    # the build's maximum beam width; many slots with a refill threshold of 0
+    ("k1_n1", 1000, 1, 1, 1, math.inf, 12, 1 / 6, 16, "f32", 8.0, 1, 6.0),
+    ("len_cap", 1000, 8, 16, 4, 2.0, 3, 1 / 6, 48, "bf16", 0.5, 0, 0.1),
+    ("max_k", 600, 128, 4, 8, 4.0, 10, 1 / 6, 12, "f32", 0.5, 0, 3.0),
+    ("many_slots", 700, 4, 512, 3, 1.5, 16, 1 / 1024, 700, "bf16", 0.5, 0, 4.0),
 ]
 
 
