@@ -384,7 +384,6 @@ __global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg,
   int* freel = claimed + k;                           // [k]
   int* nrow = freel + k;                              // [2k] child row (fill children)
   int* csrc = nrow + 2 * k;                           // [2k]
-  int* emo = csrc + 2 * k;                            // [k] drain order -> scan index
   __shared__ int wsm[NT2 / 32];
   __shared__ int s_err;
 
