@@ -61,6 +61,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// multicast variant: the box lands at the same smem offset in every CTA of
+// `mask` and completes bytes on each destination CTA's barrier at `bar`'s offset
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -111,7 +135,10 @@ __device__ __forceinline__ void load_chunk(const uint32_t (&v)[32], float (&x)[3
   }
 }
 
-template <int Mk>
+// CL = CTAs per cluster along M (1, or 2: the pair computes tiles (2mp, n) and
+// (2mp+1, n), each CTA loads half of the shared W tile and multicasts it to
+// both, halving the L2->SM operand traffic of the streamed W).
+template <int Mk, int CL>
 __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w, int R_host,
     const int* __restrict__ d_R, int K, int V, int eos, const float* __restrict__ eos_add,
@@ -122,13 +149,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = d_R ? *d_R : R_host;
   const int Mt = (R + BM - 1) / BM;
-  const int tiles = Mt * Nt;
+  const int Mu = (Mt + CL - 1) / CL;  // M units (pairs of M tiles when CL = 2)
+  const int units = Mu * Nt;
+  const int u0 = blockIdx.x / CL, ustep = gridDim.x / CL;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
   const int nk = K / BK;
+  constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1u);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], 1);
+      mbar_init(&S.empty[i], CL);  // every CTA of the cluster consumed the stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.tfull[i], 1);
@@ -143,6 +174,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CL > 1) cluster_sync();  // peers' barriers initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem_base;
 
@@ -151,13 +183,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m = t % Mt, n = t / Mt;
+      for (int u = u0; u < units; u += ustep) {
+        const int m = (u % Mu) * CL + crank, n = u / Mu;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&S.empty[st], ph ^ 1u);
           mbar_expect_tx(&S.full[st], A_BYTES + B_BYTES);
           tma_load_2d(S.a[st], &tmap_h, &S.full[st], kb * BK, m * BM);
-          tma_load_2d(S.b[st], &tmap_w, &S.full[st], kb * BK, n * BN);
+          if (CL == 1)
+            tma_load_2d(S.b[st], &tmap_w, &S.full[st], kb * BK, n * BN);
+          else
+            tma_load_2d_mc(S.b[st] + crank * (B_BYTES / CL), &tmap_w, &S.full[st], kb * BK,
+                           n * BN + crank * (BN / CL), CMASK);
           if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
@@ -170,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     if (lane == 0) {
       int st = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int u = u0; u < units; u += ustep) {
         mbar_wait(&S.tempty[acc], aph ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * BN);
@@ -181,7 +217,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)  // advance 16 bf16 = 32 B along K
             umma(d, ad + (uint64_t)((k * UK * 2) >> 4), bd + (uint64_t)((k * UK * 2) >> 4), (kb | k) != 0);
-          umma_commit(&S.empty[st]);
+          if (CL == 1)
+            umma_commit(&S.empty[st]);
+          else
+            umma_commit_mc(&S.empty[st], CMASK);  // the stage is free in every CTA's view
           if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
@@ -203,8 +242,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     int acc = 0;
     uint32_t aph = 0;
     const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m = t % Mt, n = t / Mt;
+    for (int u = u0; u < units; u += ustep) {
+      const int m = (u % Mu) * CL + crank, n = u / Mu;
       const int row = m * BM + q * 32 + lane;
       const bool live = row < R;
       const float eb = (live && eos_add) ? eos_add[row] : 0.0f;
@@ -222,13 +261,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
         continue;
       }
       float mx = -INFINITY, sm = 0.0f;
+      // TMEM -> registers double-buffered: chunk c+1's tcgen05.ld is in flight
+      // while chunk c is processed
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + half * (BN / 2));
+      uint32_t vb[2][32];
+      VS_TMEM_LD32(tbase, vb[0]);  // warp-collective: every lane, every iteration below
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) {
-        uint32_t v[32];
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");  // chunk c has landed
+        if (c + 1 < BN / 64) VS_TMEM_LD32(tbase + (uint32_t)((c + 1) * 32), vb[(c + 1) & 1]);
+        const uint32_t(&v)[32] = vb[c & 1];
         const int cc = half * (BN / 2) + c * 32;  // column within the tile
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cc);
-        VS_TMEM_LD32(taddr, v);  // warp-collective: every lane
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int col0 = n * BN + cc;
         float x[32];
         uint32_t pk[16];
@@ -279,6 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     }
   }
   __syncthreads();
+  if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it
   if (wid == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -459,7 +503,12 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
   if (2 * ((V + BN - 1) / BN) > MAXS) return VS_ERR_CONFIG;
   if (!workspace || workspace_bytes < ws_bytes(R_grid, V)) return VS_ERR_CONFIG;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, H, R_grid, K, ldh, BM) || !make_map(&mw, W, V, K, ldw, BN)) return VS_ERR_CUDA;
+  static int CLn = -1;
+  if (CLn < 0) {
+    const char* c = getenv("VS_K5_CL");  // CTAs per cluster: 2 (W multicast, default) or 1
+    CLn = (c && atoi(c) == 1) ? 1 : 2;
+  }
+  if (!make_map(&mh, H, R_grid, K, ldh, BM) || !make_map(&mw, W, V, K, ldw, BN / CLn)) return VS_ERR_CUDA;
   const int Nt = (V + BN - 1) / BN;
   float2* pms = static_cast<float2*>(workspace);
   static int sms = 0, dbg = 0;
@@ -470,27 +519,35 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
     const char* d = getenv("VS_K5_DBG");
     dbg = d ? atoi(d) : 0;
   }
-  const int tiles_max = ((R_grid + BM - 1) / BM) * Nt;
-  const int grid = tiles_max < sms ? tiles_max : sms;
+  const int units_max = ((R_grid + BM - 1) / BM + CLn - 1) / CLn * Nt;
+  int grid = units_max * CLn < sms ? units_max * CLn : sms;
+  grid -= grid % CLn;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
-#define VS_K5(MK_)                                                                                              \
-  case MK_: {                                                                                                   \
-    static bool attr = false;                                                                                   \
-    if (!attr) {                                                                                                \
-      cudaFuncSetAttribute(proj_topm_kernel<MK_>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
-                           (int)sizeof(Smem) + 1024);                                                           \
-      attr = true;                                                                                              \
-    }                                                                                                           \
-    e = vs::vs_launch(proj_topm_kernel<MK_>, dim3(grid), dim3(NTHREADS), sizeof(Smem) + 1024, st, mh, mw,       \
-                      (int)R_host, d_R, (int)K, (int)V, (int)eos, eos_add, static_cast<__nv_bfloat16*>(logits),  \
-                      ldo, pms, Nt, dbg);                                                                       \
-    break;                                                                                                      \
-  }
+#define VS_K5_ONE(MK_, CL_)                                                                                   \
+  do {                                                                                                        \
+    static bool attr = false;                                                                                 \
+    if (!attr) {                                                                                              \
+      cudaFuncSetAttribute(proj_topm_kernel<MK_, CL_>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                           (int)sizeof(Smem) + 1024);                                                         \
+      attr = true;                                                                                            \
+    }                                                                                                         \
+    e = vs::vs_launch_cluster(proj_topm_kernel<MK_, CL_>, dim3(grid), dim3(NTHREADS), sizeof(Smem) + 1024, st, \
+                              CL_, mh, mw, (int)R_host, d_R, (int)K, (int)V, (int)eos, eos_add,               \
+                              static_cast<__nv_bfloat16*>(logits), ldo, pms, Nt, dbg);                        \
+  } while (0)
+#define VS_K5(MK_)       \
+  case MK_:              \
+    if (CLn == 2)        \
+      VS_K5_ONE(MK_, 2); \
+    else                 \
+      VS_K5_ONE(MK_, 1); \
+    break;
   switch (M) {
     VS_K5(1) VS_K5(2) VS_K5(3) VS_K5(4) VS_K5(5) VS_K5(6) VS_K5(7) VS_K5(8)
   }
 #undef VS_K5
+#undef VS_K5_ONE
   if (e != cudaSuccess) return VS_ERR_CUDA;
   e = vs::vs_launch(proj_merge_kernel, dim3((R_grid + 3) / 4), dim3(128), 0, st, (int)R_host, d_R, (int)V, (int)M,
                     2 * Nt, static_cast<const float2*>(pms), static_cast<const __nv_bfloat16*>(logits), ldo, top_tok,
