@@ -77,6 +77,39 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
                "h"(mask)
                : "memory");
 }
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {  // CTA-local -> cluster address
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_expect_tx_cl(uint32_t cbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cl(void* dst, const CUtensorMap* map, uint32_t cbar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cbar), "r"(x), "r"(y)
+      : "memory");
+}
+constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)((2 * BM) >> 4) << 24);  // M = 256 across the CTA pair
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(accum));
+}
+__device__ __forceinline__ void umma2_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -135,9 +168,13 @@ __device__ __forceinline__ void load_chunk(const uint32_t (&v)[32], float (&x)[3
   }
 }
 
-// CL = CTAs per cluster along M (1, or 2: the pair computes tiles (2mp, n) and
-// (2mp+1, n), each CTA loads half of the shared W tile and multicasts it to
-// both, halving the L2->SM operand traffic of the streamed W).
+// CL = 1: one CTA per 128x256 tile.  CL = 2: CTA pairs (clusters of 2 along M)
+// compute tiles (2mp, n) and (2mp+1, n); each CTA loads half of the shared W
+// stage and multicasts it to both.  CL = 3: CTA pairs issuing one
+// tcgen05.mma.cta_group::2 (M = 256) from the leader: each CTA holds its 128
+// rows of H and 128 of the 256 W rows, all TMA completions land on the
+// leader's barriers, the leader's commits release both CTAs' stages and
+// accumulators, both epilogues drain their own TMEM.
 template <int Mk, int CL>
 __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w, int R_host,
@@ -149,28 +186,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = d_R ? *d_R : R_host;
   const int Mt = (R + BM - 1) / BM;
-  const int Mu = (Mt + CL - 1) / CL;  // M units (pairs of M tiles when CL = 2)
+  constexpr bool SM2 = CL == 3;
+  constexpr int CLX = CL == 1 ? 1 : 2;  // CTAs per cluster
+  const int Mu = (Mt + CLX - 1) / CLX;  // M units (pairs of M tiles when clustered)
   const int units = Mu * Nt;
-  const int u0 = blockIdx.x / CL, ustep = gridDim.x / CL;
-  const int crank = CL > 1 ? (int)cluster_rank() : 0;
+  const int u0 = blockIdx.x / CLX, ustep = gridDim.x / CLX;
+  const int crank = CLX > 1 ? (int)cluster_rank() : 0;
   const int nk = K / BK;
-  constexpr uint16_t CMASK = (uint16_t)((1u << CL) - 1u);
+  constexpr uint16_t CMASK = (uint16_t)((1u << CLX) - 1u);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], CL);  // every CTA of the cluster consumed the stage
+      mbar_init(&S.full[i], SM2 ? 2 : 1);            // SM2: both producers arrive (leader's copy)
+      mbar_init(&S.empty[i], CL == 2 ? 2 : 1);       // CL2: every CTA's MMA consumed the stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.tfull[i], 1);
-      mbar_init(&S.tempty[i], 8);
+      mbar_init(&S.tempty[i], SM2 ? 16 : 8);  // SM2: both CTAs' epilogue warps (leader's copy)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (wid == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&S.tmem_base))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (SM2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&S.tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&S.tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -184,16 +231,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
       int st = 0;
       uint32_t ph = 0;
       for (int u = u0; u < units; u += ustep) {
-        const int m = (u % Mu) * CL + crank, n = u / Mu;
+        const int m = (u % Mu) * CLX + crank, n = u / Mu;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&S.empty[st], ph ^ 1u);
-          mbar_expect_tx(&S.full[st], A_BYTES + B_BYTES);
-          tma_load_2d(S.a[st], &tmap_h, &S.full[st], kb * BK, m * BM);
-          if (CL == 1)
-            tma_load_2d(S.b[st], &tmap_w, &S.full[st], kb * BK, n * BN);
-          else
-            tma_load_2d_mc(S.b[st] + crank * (B_BYTES / CL), &tmap_w, &S.full[st], kb * BK,
-                           n * BN + crank * (BN / CL), CMASK);
+          if (SM2) {  // this CTA's 128 H rows and 128 W rows, completing on the leader's barrier
+            const uint32_t lbar = mapa(smem_u32(&S.full[st]), 0);
+            mbar_expect_tx_cl(lbar, A_BYTES + B_BYTES / 2);
+            tma_load_2d_cl(S.a[st], &tmap_h, lbar, kb * BK, m * BM);
+            tma_load_2d_cl(S.b[st], &tmap_w, lbar, kb * BK, n * BN + crank * (BN / 2));
+          } else {
+            mbar_expect_tx(&S.full[st], A_BYTES + B_BYTES);
+            tma_load_2d(S.a[st], &tmap_h, &S.full[st], kb * BK, m * BM);
+            if (CL == 1)
+              tma_load_2d(S.b[st], &tmap_w, &S.full[st], kb * BK, n * BN);
+            else
+              tma_load_2d_mc(S.b[st] + crank * (B_BYTES / 2), &tmap_w, &S.full[st], kb * BK,
+                             n * BN + crank * (BN / 2), CMASK);
+          }
           if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
@@ -202,8 +256,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
       }
     }
   } else if (wid == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer (SM2: the leader CTA only) =====
+    if (lane == 0 && (!SM2 || crank == 0)) {
       int st = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int u = u0; u < units; u += ustep) {
@@ -215,9 +269,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t ad = sw128_desc(smem_u32(S.a[st])), bd = sw128_desc(smem_u32(S.b[st]));
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k)  // advance 16 bf16 = 32 B along K
-            umma(d, ad + (uint64_t)((k * UK * 2) >> 4), bd + (uint64_t)((k * UK * 2) >> 4), (kb | k) != 0);
-          if (CL == 1)
+          for (int k = 0; k < BK / UK; ++k) {  // advance 16 bf16 = 32 B along K
+            if (SM2)
+              umma2(d, ad + (uint64_t)((k * UK * 2) >> 4), bd + (uint64_t)((k * UK * 2) >> 4), (kb | k) != 0);
+            else
+              umma(d, ad + (uint64_t)((k * UK * 2) >> 4), bd + (uint64_t)((k * UK * 2) >> 4), (kb | k) != 0);
+          }
+          if (SM2)
+            umma2_commit_mc(&S.empty[st], CMASK);  // both CTAs' stages are free
+          else if (CL == 1)
             umma_commit(&S.empty[st]);
           else
             umma_commit_mc(&S.empty[st], CMASK);  // the stage is free in every CTA's view
@@ -226,7 +286,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
             ph ^= 1u;
           }
         }
-        umma_commit(&S.tfull[acc]);
+        if (SM2)
+          umma2_commit_mc(&S.tfull[acc], CMASK);  // both CTAs' accumulators are ready
+        else
+          umma_commit(&S.tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           aph ^= 1u;
@@ -243,7 +306,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
     uint32_t aph = 0;
     const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
     for (int u = u0; u < units; u += ustep) {
-      const int m = (u % Mu) * CL + crank, n = u / Mu;
+      const int m = (u % Mu) * CLX + crank, n = u / Mu;
       const int row = m * BM + q * 32 + lane;
       const bool live = row < R;
       const float eb = (live && eos_add) ? eos_add[row] : 0.0f;
@@ -253,7 +316,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
       if (dbg) {  // timing knob: main loop only (results invalid)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.tempty[acc]);
+        if (lane == 0) {
+          if (SM2)
+            mbar_arrive_cl(mapa(smem_u32(&S.tempty[acc]), 0));
+          else
+            mbar_arrive(&S.tempty[acc]);
+        }
         if (++acc == 2) {
           acc = 0;
           aph ^= 1u;
@@ -311,7 +379,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.tempty[acc]);
+      if (lane == 0) {
+        if (SM2)
+          mbar_arrive_cl(mapa(smem_u32(&S.tempty[acc]), 0));  // the leader's MMA reuses both TMEMs
+        else
+          mbar_arrive(&S.tempty[acc]);
+      }
       // (sub-tile max, sum exp(x - max)): the merge also uses the max to pick
       // the only sub-tiles that can hold the row's top-M
       if (live) part_ms[(int64_t)row * (2 * Nt) + sub] = make_float2(mx, sm);
@@ -325,7 +398,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) proj_topm_kernel(
   if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it
   if (wid == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (SM2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -505,10 +581,13 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
   CUtensorMap mh, mw;
   static int CLn = -1;
   if (CLn < 0) {
-    const char* c = getenv("VS_K5_CL");  // CTAs per cluster: 2 (W multicast, default) or 1
-    CLn = (c && atoi(c) == 1) ? 1 : 2;
+    // 1: single CTAs; 2: CTA pairs multicasting W; 3: CTA pairs with cta_group::2 MMA (default)
+    const char* c = getenv("VS_K5_CL");
+    CLn = c ? atoi(c) : 2;
+    if (CLn < 1 || CLn > 3) CLn = 2;
   }
-  if (!make_map(&mh, H, R_grid, K, ldh, BM) || !make_map(&mw, W, V, K, ldw, BN / CLn)) return VS_ERR_CUDA;
+  const int CLX = CLn == 1 ? 1 : 2;
+  if (!make_map(&mh, H, R_grid, K, ldh, BM) || !make_map(&mw, W, V, K, ldw, BN / CLX)) return VS_ERR_CUDA;
   const int Nt = (V + BN - 1) / BN;
   float2* pms = static_cast<float2*>(workspace);
   static int sms = 0, dbg = 0;
@@ -519,9 +598,9 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
     const char* d = getenv("VS_K5_DBG");
     dbg = d ? atoi(d) : 0;
   }
-  const int units_max = ((R_grid + BM - 1) / BM + CLn - 1) / CLn * Nt;
-  int grid = units_max * CLn < sms ? units_max * CLn : sms;
-  grid -= grid % CLn;
+  const int units_max = ((R_grid + BM - 1) / BM + CLX - 1) / CLX * Nt;
+  int grid = units_max * CLX < sms ? units_max * CLX : sms;
+  grid -= grid % CLX;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaErrorInvalidValue;
 #define VS_K5_ONE(MK_, CL_)                                                                                   \
@@ -533,12 +612,14 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
       attr = true;                                                                                            \
     }                                                                                                         \
     e = vs::vs_launch_cluster(proj_topm_kernel<MK_, CL_>, dim3(grid), dim3(NTHREADS), sizeof(Smem) + 1024, st, \
-                              CL_, mh, mw, (int)R_host, d_R, (int)K, (int)V, (int)eos, eos_add,               \
+                              CL_ == 1 ? 1 : 2, mh, mw, (int)R_host, d_R, (int)K, (int)V, (int)eos, eos_add,               \
                               static_cast<__nv_bfloat16*>(logits), ldo, pms, Nt, dbg);                        \
   } while (0)
 #define VS_K5(MK_)       \
   case MK_:              \
-    if (CLn == 2)        \
+    if (CLn == 3)        \
+      VS_K5_ONE(MK_, 3); \
+    else if (CLn == 2)   \
       VS_K5_ONE(MK_, 2); \
     else                 \
       VS_K5_ONE(MK_, 1); \
