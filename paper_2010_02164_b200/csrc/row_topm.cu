@@ -23,6 +23,7 @@
 // value.  Rows that cannot be proven fall back to an exact warp radix select
 // over 64-bit keys.  Every decision is a pure function of the row.
 #include "common.cuh"
+#include "select_common.cuh"
 #include <cstdlib>
 
 namespace vs {
@@ -106,6 +107,11 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
   return e;
 }
+// The running max m of the online log-sum-exp is warp-uniform and lazily raised:
+// it only moves when some element exceeds m + RESCALE_MARGIN, so exp(x - m) stays
+// <= e^16 (sums stay far from fp32 overflow) and the hot loop needs no per-vector
+// rescale (an exponential per vector saved).
+constexpr float RESCALE_MARGIN = 16.0f;
 
 // logit key: larger = earlier in (value desc, token asc).
 __device__ __forceinline__ uint64_t vkey(float x, int tok) {
@@ -239,6 +245,50 @@ __device__ __forceinline__ Cand append_fast(Cand c, float x0, float x1, float x2
   return c;
 }
 
+// Register top-list (Meff <= 32): lane j holds the j-th largest key seen so far
+// and θ is always the exact Meff-th key, so no buffer flushes and the fewest
+// possible candidate entries (≈ M·ln(V/M) per row).
+struct TopList {
+  uint64_t tk;  // this lane's entry (0 = empty)
+};
+__device__ __forceinline__ void tl_insert(TopList& t, Cand& c, uint64_t k, int Meff, int lane) {
+  const int pos = __popc(__ballot_sync(FULL, t.tk > k));
+  if (pos >= Meff) return;  // uniform
+  const uint64_t up = (uint64_t)__shfl_up_sync(FULL, (unsigned long long)t.tk, 1);
+  t.tk = lane == pos ? k : (lane > pos && lane < Meff ? up : t.tk);
+  const uint64_t last = (uint64_t)__shfl_sync(FULL, (unsigned long long)t.tk, Meff - 1);
+  if (last > c.theta) {
+    c.theta = last;
+    c.theta_x = unord_f32((uint32_t)(last >> 32));
+  }
+}
+// Insert this lane's elements >= θx of one vector (warp-synchronous; taken only
+// when some lane's vector max reaches θx): one ballot round per pending element.
+__device__ __forceinline__ void tl_append(TopList& t, Cand& c, const float (&x)[8], int n, int tok0,
+                                          int Meff) {
+  const int lane = threadIdx.x & 31;
+  unsigned em = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < n && x[j] >= c.theta_x) em |= 1u << j;
+  while (__any_sync(FULL, em != 0)) {
+    const int j = em ? __ffs(em) - 1 : 0;
+    float xj = x[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) xj = (j == q) ? x[q] : xj;
+    const uint64_t k = vkey(xj, tok0 + j);
+    const bool cnd = em != 0 && k > c.theta;
+    em &= em - 1;
+    unsigned b = __ballot_sync(FULL, cnd);
+    while (b) {
+      const int src = __ffs(b) - 1;
+      b &= b - 1;
+      const uint64_t kk = (uint64_t)__shfl_sync(FULL, (unsigned long long)k, src);
+      if (kk > c.theta) tl_insert(t, c, kk, Meff, lane);
+    }
+  }
+}
+
 // Warps per row from the live row count: minimise the makespan
 // ceil(R*W/T) * (c0 + 1/W) over W in {1,2,4,8} (T = resident warps, c0 =
 // per-task boot/epilogue cost relative to streaming a whole row) — balances
@@ -267,7 +317,13 @@ struct PartSmem {  // per-warp results exchanged between the W warps of a row
 
 // W warps per row (W in {1,2,4}; 4/W rows per CTA).  Warp `part` of a row
 // streams vectors [part*seg, (part+1)*seg); the row's leader warp combines.
-template <typename T, int U, int MINB>
+// TL: candidates in a register top-list (Meff <= 32) instead of the flushed
+// shared-memory buffer.  NS > 0 (ring): the warp's slice streams through a
+// private ring of NS shared-memory chunks of U·512 B filled by cp.async.bulk
+// (one lane issues, per-chunk mbarriers) instead of register double-buffering,
+// so NS-1 chunks stay in flight while one is reduced and no registers are held
+// by loads.
+template <typename T, int U, int MINB, bool TL, int NS>
 __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
@@ -275,7 +331,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     int warps_per_sm, float c0) {
   VS_PDL_ENTRY();
   constexpr int VEC = 16 / sizeof(T);
-  __shared__ uint64_t sbuf[WPC][CAPW];
+  constexpr int CAP = TL ? 128 : CAPW;  // TL: <= 4 parts x 32 keys at the merge
+  __shared__ uint64_t sbuf[WPC][CAP];
+  __shared__ uint64_t rbar[WPC][NS > 0 ? NS : 1];
   __shared__ uint64_t ssel[WPC][VS_MAX_M];
   __shared__ unsigned shist[WPC][256];
   __shared__ PartSmem spart[WPC];
@@ -296,34 +354,84 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   // needs no -inf guards: ex2(x*log2e - m*log2e) is 0 for x = -inf and the
   // branchless rescale ex2((m_old - m_new)*log2e) is 0 on the first vector.
   constexpr float M_FLOOR = -1e30f;
-  float m = M_FLOOR;
+  float m = M_FLOOR, m_thr = M_FLOOR + RESCALE_MARGIN;  // warp-uniform (see RESCALE_MARGIN)
+  unsigned long long nml2 = pk2(-M_FLOOR * VS_LOG2E, -M_FLOOR * VS_LOG2E);
   unsigned long long s01 = pk2(0.0f, 0.0f);  // (even, odd) partial sums of exp(x - m)
   const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
   Cand c{0ull, -INFINITY, 0};
+  TopList tl{0ull};
 
+  // Candidate path of one vector (warp-synchronous).
+  auto cand = [&](const float (&x)[VEC], int n, int tok0) {
+#ifndef K1_ABL_NOCAND  // ablation build only (tools/k1_ablate.sh)
+    if (TL) {
+      if constexpr (VEC == 8) {
+        tl_append(tl, c, reinterpret_cast<const float(&)[8]>(x), n, tok0, Meff);
+      } else {
+        const float x8[8] = {x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
+                             -INFINITY};
+        tl_append(tl, c, x8, n, tok0, Meff);
+      }
+    } else if (VEC == 8)
+      c = append_fast<true>(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
+                            x[VEC > 6 ? 6 : 0], x[VEC > 7 ? 7 : 0], n, tok0, buf, sel, Meff, flush_at);
+    else
+      c = append_fast<true>(c, x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
+                            -INFINITY, n, tok0, buf, sel, Meff, flush_at);
+#endif
+  };
   auto consume = [&](const float (&x)[VEC], int n, int tok0) {
     float cm = x[0];
 #pragma unroll
     for (int j = 1; j < VEC; ++j) cm = fmaxf(cm, x[j]);
-    const float mn = fmaxf(m, cm);
-    const float sc = ex2f((m - mn) * VS_LOG2E);  // branchless online rescale
-    s01 = mul2(s01, pk2(sc, sc));
-    m = mn;
-    const float nml = -m * VS_LOG2E;
-    const unsigned long long nml2 = pk2(nml, nml);
+    // One warp vote guards both rare paths: θx <= (warp max so far) <= m_thr, so
+    // an element above m_thr also passes the candidate test.
+    if (__any_sync(FULL, cm >= c.theta_x)) {
+      if (__any_sync(FULL, cm > m_thr)) {  // raise the shared max, rescale the sums
+        float mw = cm;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mw = fmaxf(mw, __shfl_xor_sync(FULL, mw, o));
+        const float sc = ex2f((m - mw) * VS_LOG2E);
+        s01 = mul2(s01, pk2(sc, sc));
+        m = mw;
+        m_thr = m + RESCALE_MARGIN;
+        nml2 = pk2(-m * VS_LOG2E, -m * VS_LOG2E);
+      }
+      cand(x, n, tok0);
+    }
 #pragma unroll
     for (int j = 0; j < VEC; j += 2) {
+      const unsigned long long t = fma2(pk2(x[j], x[j + 1]), L2E2, nml2);  // FFMA2: (x - m)*log2e
+#ifdef K1_ABL_NOEXP
+      s01 = add2(s01, t);  // ablation build only (tools/k1_ablate.sh)
+#else
       float t0, t1;
-      up2(fma2(pk2(x[j], x[j + 1]), L2E2, nml2), t0, t1);  // FFMA2: x*log2e - m*log2e
-      s01 = add2(s01, pk2(ex2f(t0), ex2f(t1)));          // FADD2
+      up2(t, t0, t1);
+      s01 = add2(s01, pk2(ex2f(t0), ex2f(t1)));  // MUFU.EX2 + FADD2
+#endif
     }
-    if (__any_sync(FULL, cm >= c.theta_x)) {
-      if (VEC == 8)
-        c = append_fast<true>(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
-                        x[VEC > 6 ? 6 : 0], x[VEC > 7 ? 7 : 0], n, tok0, buf, sel, Meff, flush_at);
-      else
-        c = append_fast<true>(c, x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
-                        -INFINITY, n, tok0, buf, sel, Meff, flush_at);
+  };
+
+  // θ bootstrap from the lane maxima of the first two batches: θ = M-th largest
+  // (a bitonic shuffle sort), and the shared max m starts at the largest.
+  auto boot = [&](float lm) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const float o = __shfl_xor_sync(FULL, lm, j);
+        lm = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(lm, o) : fminf(lm, o);
+      }
+    const float t0 = __shfl_sync(FULL, lm, Meff - 1);
+    const float m0 = __shfl_sync(FULL, lm, 0);
+    if (m0 > M_FLOOR) {
+      m = m0;
+      m_thr = m0 + RESCALE_MARGIN;
+      nml2 = pk2(-m * VS_LOG2E, -m * VS_LOG2E);
+    }
+    if (t0 != -INFINITY) {
+      c.theta = (uint64_t)ord_f32(t0) << 32;  // (t0, token = +inf): x == t0 still passes
+      c.theta_x = t0;
     }
   };
 
@@ -333,94 +441,152 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const int seg = (ntot + W - 1) / W;
     const int v0 = min(ntot, part * seg), v1 = min(ntot, v0 + seg);
     const uint4* __restrict__ vrow = reinterpret_cast<const uint4*>(row);
-    constexpr int BATCH = 32 * U;  // vectors per warp per batch
-    uint4 cur[U], nxt[U];
+    if constexpr (NS > 0) {
+      constexpr int CH = 32 * U;  // vectors per chunk
+      extern __shared__ __align__(128) unsigned char ring_smem[];
+      uint4* stg = reinterpret_cast<uint4*>(ring_smem) + (size_t)wid * NS * CH;
+      uint64_t* bars = rbar[wid];
+      const int nvt = v1 - v0, nch = (nvt + CH - 1) / CH;
+      const uint64_t pol = tk::policy_evict_first();
+      if (lane == 0) {
+        for (int q = 0; q < NS; ++q) tk::mbar_init(&bars[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncwarp();
+      auto issue = [&](int ch) {
+        const int q = ch % NS;
+        const unsigned bytes = (unsigned)min(CH, nvt - ch * CH) * 16u;
+        tk::mbar_expect_tx(&bars[q], bytes);
+        tk::bulk_g2s(stg + q * CH, vrow + v0 + ch * CH, bytes, &bars[q], pol);
+      };
+      if (lane == 0)
+        for (int ch = 0; ch < min(NS, nch); ++ch) issue(ch);
+      if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 chunks
+        float lm = -INFINITY;
+        for (int ch = 0; ch < min(2, nch); ++ch) {
+          tk::mbar_wait(&bars[ch], 0);
+          const uint4* sv = stg + ch * CH;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = v0 + lane + 32 * u;
-      if (i < v1) cur[u] = ldg_stream(vrow + i);
-    }
+          for (int u = 0; u < U; ++u) {
+            const int i = lane + 32 * u;
+            if (ch * CH + i < nvt) {
+              float x[VEC];
+              unpack<T>(sv[i], x);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = v0 + BATCH + lane + 32 * u;
-      if (i < v1) nxt[u] = ldg_stream(vrow + i);
-    }
-    if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 batches
-      float lm = -INFINITY;
+              for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+            }
+          }
+        }
+        boot(lm);
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        const int q = ch % NS;
+        tk::mbar_wait(&bars[q], (unsigned)(ch / NS) & 1u);
+        const uint4* sv = stg + q * CH;
+        const int nv = min(CH, nvt - ch * CH), tok = (v0 + ch * CH) * VEC;
+        if (nv == CH) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            float x[VEC];
+            unpack<T>(sv[lane + 32 * u], x);
+            consume(x, VEC, tok + (lane + 32 * u) * VEC);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = lane + 32 * u;
+            if (__any_sync(FULL, i < nv)) {
+              float x[VEC];
+              if (i < nv) unpack<T>(sv[i], x);
+              else
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) x[j] = -INFINITY;
+              consume(x, VEC, tok + i * VEC);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0 && ch + NS < nch) issue(ch + NS);
+      }
+    } else {
+      constexpr int BATCH = 32 * U;  // vectors per warp per batch
+      uint4 cur[U], nxt[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        float x[VEC];
-        if (v0 + lane + 32 * u < v1) {
-          unpack<T>(cur[u], x);
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
-        }
-        if (v0 + BATCH + lane + 32 * u < v1) {
-          unpack<T>(nxt[u], x);
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
-        }
-      }
-#pragma unroll
-      for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          const float o = __shfl_xor_sync(FULL, lm, j);
-          lm = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(lm, o) : fminf(lm, o);
-        }
-      const float t0 = __shfl_sync(FULL, lm, Meff - 1);
-      if (t0 != -INFINITY) {
-        c.theta = (uint64_t)ord_f32(t0) << 32;  // (t0, token = +inf): x == t0 still passes
-        c.theta_x = t0;
-      }
-    }
-    int base = v0;
-    const int pf_dist = 2 * BATCH * pf_batches;  // vectors ahead of the demand loads
-    if (lane == 0 && pf_batches > 0) {  // prime the L2 prefetch window
-      const int p1 = min(v1, v0 + pf_dist);
-      if (p1 > v0 + 2 * BATCH) l2_prefetch(vrow + v0 + 2 * BATCH, (unsigned)(p1 - v0 - 2 * BATCH) * 16u);
-    }
-    // full double-batches: no per-vector bounds checks
-    for (; base + 2 * BATCH <= v1; base += 2 * BATCH) {
-      if (lane == 0 && pf_batches > 0) {
-        const int p0 = base + pf_dist, p1 = min(v1, p0 + 2 * BATCH);
-        if (p1 > p0) l2_prefetch(vrow + p0, (unsigned)(p1 - p0) * 16u);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        float x[VEC];
-        unpack<T>(cur[u], x);
-        consume(x, VEC, (base + lane + 32 * u) * VEC);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + 2 * BATCH + lane + 32 * u;
+        const int i = v0 + lane + 32 * u;
         if (i < v1) cur[u] = ldg_stream(vrow + i);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        float x[VEC];
-        unpack<T>(nxt[u], x);
-        consume(x, VEC, (base + BATCH + lane + 32 * u) * VEC);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + 3 * BATCH + lane + 32 * u;
+        const int i = v0 + BATCH + lane + 32 * u;
         if (i < v1) nxt[u] = ldg_stream(vrow + i);
       }
-    }
-    // remainder (< 2 batches, already loaded into cur / nxt): checked
-    for (int h = 0; h < 2; ++h) {
+      if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 batches
+        float lm = -INFINITY;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + h * BATCH + lane + 32 * u;
-        if (__any_sync(FULL, i < v1)) {
+        for (int u = 0; u < U; ++u) {
           float x[VEC];
-          if (i < v1) unpack<T>(h ? nxt[u] : cur[u], x);
-          else
+          if (v0 + lane + 32 * u < v1) {
+            unpack<T>(cur[u], x);
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) x[j] = -INFINITY;
-          consume(x, VEC, i * VEC);
+            for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+          }
+          if (v0 + BATCH + lane + 32 * u < v1) {
+            unpack<T>(nxt[u], x);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+          }
+        }
+        boot(lm);
+      }
+      int base = v0;
+      const int pf_dist = 2 * BATCH * pf_batches;  // vectors ahead of the demand loads
+      if (lane == 0 && pf_batches > 0) {  // prime the L2 prefetch window
+        const int p1 = min(v1, v0 + pf_dist);
+        if (p1 > v0 + 2 * BATCH) l2_prefetch(vrow + v0 + 2 * BATCH, (unsigned)(p1 - v0 - 2 * BATCH) * 16u);
+      }
+      // full double-batches: no per-vector bounds checks
+      for (; base + 2 * BATCH <= v1; base += 2 * BATCH) {
+        if (lane == 0 && pf_batches > 0) {
+          const int p0 = base + pf_dist, p1 = min(v1, p0 + 2 * BATCH);
+          if (p1 > p0) l2_prefetch(vrow + p0, (unsigned)(p1 - p0) * 16u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float x[VEC];
+          unpack<T>(cur[u], x);
+          consume(x, VEC, (base + lane + 32 * u) * VEC);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + 2 * BATCH + lane + 32 * u;
+          if (i < v1) cur[u] = ldg_stream(vrow + i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float x[VEC];
+          unpack<T>(nxt[u], x);
+          consume(x, VEC, (base + BATCH + lane + 32 * u) * VEC);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + 3 * BATCH + lane + 32 * u;
+          if (i < v1) nxt[u] = ldg_stream(vrow + i);
+        }
+      }
+      // remainder (< 2 batches, already loaded into cur / nxt): checked
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + h * BATCH + lane + 32 * u;
+          if (__any_sync(FULL, i < v1)) {
+            float x[VEC];
+            if (i < v1) unpack<T>(h ? nxt[u] : cur[u], x);
+            else
+#pragma unroll
+              for (int j = 0; j < VEC; ++j) x[j] = -INFINITY;
+            consume(x, VEC, i * VEC);
+          }
         }
       }
     }
@@ -434,6 +600,12 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         consume(x, 1, i);
       }
     }
+  }
+  if (TL) {  // hand the list to the common epilogue as a sorted buffer
+    const bool has = lane < Meff && tl.tk != 0ull;
+    if (has) buf[lane] = tl.tk;
+    c.cnt = __popc(__ballot_sync(FULL, has));
+    __syncwarp();
   }
   // ---- per-warp lse partial -> exchange --------------------------------------------
   float s;
@@ -480,7 +652,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     for (int q = 1; q < W; ++q) {
       const int nq = spart[leader + q].cnt;
       const uint64_t* bq = sbuf[leader + q];
-      if (c.cnt + nq > CAPW) {  // compact own buffer first (exact: by final key)
+      if (c.cnt + nq > CAP) {  // compact own buffer first (exact: by final key)
         __syncwarp();
         warp_select(buf, c.cnt, Meff, sel);
         c.cnt = Meff;
@@ -510,6 +682,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
       ok = lp < t_lp || (lp == t_lp && (th_tok == -1 || th_tok >= t_tok));
     }
   }
+#ifdef K1_ABL_NOCAND
+  ok = true;
+#endif
   if (!ok) {
     warp_exact_select<T>(row, V, lse, Meff, shist[wid], buf, sel);
     if (lane == 0 && fb_count) atomicAdd(fb_count, 1);
@@ -527,6 +702,16 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   if (lane == 0 && row_lse) row_lse[r] = lse;
 }
 
+// Opt a kernel in to its dynamic shared memory once (static + dynamic > 48 KB).
+void allow_dyn_smem(const void* kern, size_t dsm) {
+  static const void* done[64];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (done[i] == kern) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (n < 64) done[n++] = kern;
+}
+
 template <typename T>
 int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* d_R, int rows, int* top_tok,
            float* top_logp, float* row_lse, int* fb, int norm, cudaStream_t st) {
@@ -539,8 +724,11 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   static int variant = -1, flush_min = FLUSH_MIN, pf = 0;  // knobs: VS_K1_VARIANT/_FLUSH/_PF/_C0
+  static int tl_mode = 1;                                   // VS_K1_TL=0: buffered candidates
   static float c0 = PICKW_C0;
   if (variant < 0) {
+    const char* y = getenv("VS_K1_TL");
+    if (y) tl_mode = atoi(y);
     const char* c = getenv("VS_K1_C0");
     if (c) c0 = (float)atof(c);
     const char* q = getenv("VS_K1_PF");
@@ -550,7 +738,9 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     const char* f = getenv("VS_K1_FLUSH");
     if (f) flush_min = atoi(f);
   }
-  const int ctas_per_sm = variant == 0 ? 2 : (variant == 3 ? 3 : 4);
+  // variants: 0/1/3 register double-buffering (U, CTAs/SM) = (4,2) (2,4) (3,3);
+  // 4/5 shared-memory ring (U, NS, CTAs/SM) = (4,3,3) (2,4,4)
+  const int ctas_per_sm = variant == 0 ? 2 : ((variant == 3 || variant == 4) ? 3 : 4);
   const int Tw = sms * ctas_per_sm * WPC;
   // grid covers the worst case over the W the kernel will pick from the live R
   int grid;
@@ -568,15 +758,28 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     grid = (rows * pick_w(rows, V, Tw, c0) + WPC - 1) / WPC;
   }
   const T* p = static_cast<const T*>(logits);
-#define VS_K1_LAUNCH(U_, B_)                                                                            \
-  vs::vs_launch(row_lse_topm_warp_kernel<T, U_, B_>, dim3(grid), dim3(WPC * 32), 0, st, p, ld, V, M, R_host, d_R, top_tok, \
-                                                                 top_logp, row_lse, fb, norm, sms, flush_min, pf, \
-                                                                 ctas_per_sm * WPC, c0)
+  const bool TLm = (M < V ? M : V) <= 32 && tl_mode;
+#define VS_K1_LAUNCH(U_, B_, TL_, NS_)                                                                  \
+  do {                                                                                                   \
+    auto kern = row_lse_topm_warp_kernel<T, U_, B_, TL_, NS_>;                                           \
+    const size_t dsm = (size_t)WPC * NS_ * 32 * U_ * 16;                                                \
+    if (dsm > 0) allow_dyn_smem((const void*)kern, dsm);                                                  \
+    vs::vs_launch(kern, dim3(grid), dim3(WPC * 32), dsm, st, p, ld, V, M, R_host, d_R, top_tok, top_logp,    \
+                  row_lse, fb, norm, sms, flush_min, pf, ctas_per_sm * WPC, c0);                         \
+  } while (0)
+#define VS_K1_LAUNCH3(U_, B_, NS_)     \
+  if (TLm)                             \
+    VS_K1_LAUNCH(U_, B_, true, NS_);   \
+  else                                 \
+    VS_K1_LAUNCH(U_, B_, false, NS_);
   switch (variant) {
-    case 0: VS_K1_LAUNCH(4, 2); break;
-    case 3: VS_K1_LAUNCH(3, 3); break;
-    default: VS_K1_LAUNCH(2, 4); break;
+    case 0: VS_K1_LAUNCH3(4, 2, 0); break;
+    case 3: VS_K1_LAUNCH3(3, 3, 0); break;
+    case 4: VS_K1_LAUNCH3(4, 3, 3); break;
+    case 5: VS_K1_LAUNCH3(2, 4, 4); break;
+    default: VS_K1_LAUNCH3(2, 4, 0); break;
   }
+#undef VS_K1_LAUNCH3
 #undef VS_K1_LAUNCH
   VS_CUDA_RET();
 }
