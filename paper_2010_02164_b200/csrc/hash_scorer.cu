@@ -31,8 +31,10 @@ __device__ __forceinline__ float hash_logit(uint32_t key, int v, float scale, in
   if (power == 0) {  // log-like: -scale * (e + f), u' = ((bits>>8)+1) * 2^-24 = 2^e (1+f)
     const float u1 = __fmul_rn((float)((bits >> 8) + 1u), 5.9604644775390625e-08f);
     const uint32_t ub = __float_as_uint(u1);
-    const float e = (float)((int)(ub >> 23) - 127);
-    const float f = __fmul_rn((float)(ub & 0x7FFFFFu), 1.1920928955078125e-07f);
+    // e and f without int->float conversions (XU pipe): both are exact —
+    // e via the 1.5*2^23 shifter, f = (1 + m*2^-23) - 1 (Sterbenz).
+    const float e = __fsub_rn(__int_as_float(0x4B400000 + (int)(ub >> 23) - 127), 12582912.0f);
+    const float f = __fsub_rn(__uint_as_float(0x3F800000u | (ub & 0x7FFFFFu)), 1.0f);
     return __fmul_rn(-scale, __fadd_rn(e, f));
   }
   float u = __fmul_rn((float)(bits >> 8), 5.9604644775390625e-08f);  // * 2^-24, exact

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "select_common.cuh"
 #include <cstdlib>
+#include <type_traits>
 
 namespace vs {
 namespace {
@@ -247,46 +248,99 @@ __device__ __forceinline__ Cand append_fast(Cand c, float x0, float x1, float x2
 
 // Register top-list (Meff <= 32): lane j holds the j-th largest key seen so far
 // and θ is always the exact Meff-th key, so no buffer flushes and the fewest
-// possible candidate entries (≈ M·ln(V/M) per row).
-struct TopList {
-  uint64_t tk;  // this lane's entry (0 = empty)
+// possible candidate entries (≈ M·ln(V/M) per row).  Keys are 64-bit
+// (ord(x) << 32 | ~token) or, for bf16 rows with |V| < 65536, 32-bit
+// (ord16(x) << 16 | 0xFFFF - token): same order, half the shuffles/compares.
+// A key whose token field is 0 means "token +inf" (x == θx still passes).
+template <typename K>
+struct KeyOps;
+template <>
+struct KeyOps<uint64_t> {
+  static __device__ __forceinline__ uint64_t key(float x, int tok) { return vkey(x, tok); }
+  static __device__ __forceinline__ uint64_t bound(float x) { return (uint64_t)ord_f32(x) << 32; }
+  static __device__ __forceinline__ float val(uint64_t k) { return unord_f32((uint32_t)(k >> 32)); }
+  static __device__ __forceinline__ uint64_t to64(uint64_t k) { return k; }
 };
-__device__ __forceinline__ void tl_insert(TopList& t, Cand& c, uint64_t k, int Meff, int lane) {
+template <>
+struct KeyOps<uint32_t> {
+  static __device__ __forceinline__ uint32_t key(float x, int tok) {
+    return (ord_f32(x) & 0xFFFF0000u) | (0xFFFFu - (uint32_t)tok);
+  }
+  static __device__ __forceinline__ uint32_t bound(float x) { return ord_f32(x) & 0xFFFF0000u; }
+  static __device__ __forceinline__ float val(uint32_t k) {
+    return unord_f32((k & 0xFFFF0000u) | ((k & 0x80000000u) ? 0u : 0xFFFFu));
+  }
+  static __device__ __forceinline__ uint64_t to64(uint32_t k) {
+    if (k == 0u) return 0ull;
+    const uint64_t hi = (uint64_t)ord_f32(val(k)) << 32;
+    return (k & 0xFFFFu) ? hi | (uint64_t)(0xffffffffu - (0xFFFFu - (k & 0xFFFFu))) : hi;
+  }
+};
+template <typename K>
+struct TopList {
+  K tk;        // this lane's entry (0 = empty)
+  K theta;     // exact Meff-th key (warp-uniform; 0 = everything passes)
+  float theta_x;
+};
+template <typename K>
+__device__ __forceinline__ void tl_insert(TopList<K>& t, K k, int Meff, int lane) {
   const int pos = __popc(__ballot_sync(FULL, t.tk > k));
-  if (pos >= Meff) return;  // uniform
-  const uint64_t up = (uint64_t)__shfl_up_sync(FULL, (unsigned long long)t.tk, 1);
+  if (pos >= Meff || __any_sync(FULL, t.tk == k)) return;  // uniform (== : a seeded key seen again)
+  const K up = (K)__shfl_up_sync(FULL, t.tk, 1);
   t.tk = lane == pos ? k : (lane > pos && lane < Meff ? up : t.tk);
-  const uint64_t last = (uint64_t)__shfl_sync(FULL, (unsigned long long)t.tk, Meff - 1);
-  if (last > c.theta) {
-    c.theta = last;
-    c.theta_x = unord_f32((uint32_t)(last >> 32));
+  const K last = (K)__shfl_sync(FULL, t.tk, Meff - 1);
+  if (last > t.theta) {
+    t.theta = last;
+    t.theta_x = KeyOps<K>::val(last);
   }
 }
 // Insert this lane's elements >= θx of one vector (warp-synchronous; taken only
 // when some lane's vector max reaches θx): one ballot round per pending element.
-__device__ __forceinline__ void tl_append(TopList& t, Cand& c, const float (&x)[8], int n, int tok0,
-                                          int Meff) {
+template <typename K>
+__device__ __forceinline__ void tl_append(TopList<K>& t, const float (&x)[8], int n, int tok0, int Meff) {
   const int lane = threadIdx.x & 31;
   unsigned em = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    if (j < n && x[j] >= c.theta_x) em |= 1u << j;
+    if (j < n && x[j] >= t.theta_x) em |= 1u << j;
   while (__any_sync(FULL, em != 0)) {
     const int j = em ? __ffs(em) - 1 : 0;
     float xj = x[0];
 #pragma unroll
     for (int q = 1; q < 8; ++q) xj = (j == q) ? x[q] : xj;
-    const uint64_t k = vkey(xj, tok0 + j);
-    const bool cnd = em != 0 && k > c.theta;
+    const K k = KeyOps<K>::key(xj, tok0 + j);
+    const bool cnd = em != 0 && k > t.theta;
     em &= em - 1;
     unsigned b = __ballot_sync(FULL, cnd);
     while (b) {
       const int src = __ffs(b) - 1;
       b &= b - 1;
-      const uint64_t kk = (uint64_t)__shfl_sync(FULL, (unsigned long long)k, src);
-      if (kk > c.theta) tl_insert(t, c, kk, Meff, lane);
+      const K kk = (K)__shfl_sync(FULL, k, src);
+      if (kk > t.theta) tl_insert(t, kk, Meff, lane);
     }
   }
+}
+// Seed the list from the 32 lane maxima (value, first token) of the bootstrap
+// window: a bitonic sort leaves the top Meff in lanes 0..Meff-1, i.e. exactly
+// the state after inserting them.  Returns the window maximum.
+template <typename K>
+__device__ __forceinline__ float tl_seed(TopList<K>& t, float lm, int lt, int Meff, int lane) {
+  K k = lm == -INFINITY ? (K)0 : KeyOps<K>::key(lm, lt);
+#pragma unroll
+  for (int s = 2; s <= 32; s <<= 1)
+#pragma unroll
+    for (int j = s >> 1; j > 0; j >>= 1) {
+      const K o = (K)__shfl_xor_sync(FULL, k, j);
+      k = (((lane & s) == 0) == ((lane & j) == 0)) ? (k > o ? k : o) : (k < o ? k : o);
+    }
+  t.tk = lane < Meff ? k : (K)0;
+  const K last = (K)__shfl_sync(FULL, k, Meff - 1);
+  if (last != (K)0) {
+    t.theta = last;
+    t.theta_x = KeyOps<K>::val(last);
+  }
+  const K top = (K)__shfl_sync(FULL, k, 0);
+  return top ? KeyOps<K>::val(top) : -INFINITY;
 }
 
 // Warps per row from the live row count: minimise the makespan
@@ -317,13 +371,13 @@ struct PartSmem {  // per-warp results exchanged between the W warps of a row
 
 // W warps per row (W in {1,2,4}; 4/W rows per CTA).  Warp `part` of a row
 // streams vectors [part*seg, (part+1)*seg); the row's leader warp combines.
-// TL: candidates in a register top-list (Meff <= 32) instead of the flushed
-// shared-memory buffer.  NS > 0 (ring): the warp's slice streams through a
+// TLK: 0 = candidates in the flushed shared-memory buffer; 1/2 = register
+// top-list (Meff <= 32) with 64/32-bit keys.  NS > 0 (ring): the warp's slice streams through a
 // private ring of NS shared-memory chunks of U·512 B filled by cp.async.bulk
 // (one lane issues, per-chunk mbarriers) instead of register double-buffering,
 // so NS-1 chunks stay in flight while one is reduced and no registers are held
 // by loads.
-template <typename T, int U, int MINB, bool TL, int NS>
+template <typename T, int U, int MINB, int TLK, int NS>
 __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     const T* __restrict__ logits, int64_t ld, int V, int M, int R_host, const int* __restrict__ d_R,
     int* __restrict__ top_tok, float* __restrict__ top_logp, float* __restrict__ row_lse,
@@ -331,6 +385,8 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     int warps_per_sm, float c0) {
   VS_PDL_ENTRY();
   constexpr int VEC = 16 / sizeof(T);
+  constexpr bool TL = TLK > 0;
+  using K = typename std::conditional<TLK == 2, uint32_t, uint64_t>::type;
   constexpr int CAP = TL ? 128 : CAPW;  // TL: <= 4 parts x 32 keys at the merge
   __shared__ uint64_t sbuf[WPC][CAP];
   __shared__ uint64_t rbar[WPC][NS > 0 ? NS : 1];
@@ -359,18 +415,18 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   unsigned long long s01 = pk2(0.0f, 0.0f);  // (even, odd) partial sums of exp(x - m)
   const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
   Cand c{0ull, -INFINITY, 0};
-  TopList tl{0ull};
+  TopList<K> tl{(K)0, (K)0, -INFINITY};
 
   // Candidate path of one vector (warp-synchronous).
   auto cand = [&](const float (&x)[VEC], int n, int tok0) {
 #ifndef K1_ABL_NOCAND  // ablation build only (tools/k1_ablate.sh)
     if (TL) {
       if constexpr (VEC == 8) {
-        tl_append(tl, c, reinterpret_cast<const float(&)[8]>(x), n, tok0, Meff);
+        tl_append(tl, reinterpret_cast<const float(&)[8]>(x), n, tok0, Meff);
       } else {
         const float x8[8] = {x[0], x[1 % VEC], x[2 % VEC], x[3 % VEC], -INFINITY, -INFINITY, -INFINITY,
                              -INFINITY};
-        tl_append(tl, c, x8, n, tok0, Meff);
+        tl_append(tl, x8, n, tok0, Meff);
       }
     } else if (VEC == 8)
       c = append_fast<true>(c, x[0], x[1], x[2], x[3], x[VEC > 4 ? 4 : 0], x[VEC > 5 ? 5 : 0],
@@ -386,7 +442,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     for (int j = 1; j < VEC; ++j) cm = fmaxf(cm, x[j]);
     // One warp vote guards both rare paths: θx <= (warp max so far) <= m_thr, so
     // an element above m_thr also passes the candidate test.
-    if (__any_sync(FULL, cm >= c.theta_x)) {
+    if (__any_sync(FULL, cm >= (TL ? tl.theta_x : c.theta_x))) {
       if (__any_sync(FULL, cm > m_thr)) {  // raise the shared max, rescale the sums
         float mw = cm;
 #pragma unroll
@@ -412,27 +468,42 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     }
   };
 
-  // θ bootstrap from the lane maxima of the first two batches: θ = M-th largest
-  // (a bitonic shuffle sort), and the shared max m starts at the largest.
-  auto boot = [&](float lm) {
+  // θ bootstrap from the lane maxima (value, first token) of the first two
+  // batches: the top-list is seeded with the top Meff of them (buffer mode: θ =
+  // the Meff-th largest value), and the shared max m starts at the largest.
+  auto boot = [&](float lm, int lt) {
+    float m0;
+    if constexpr (TL) {
+      m0 = tl_seed(tl, lm, lt, Meff, lane);
+    } else {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1)
+      for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const float o = __shfl_xor_sync(FULL, lm, j);
-        lm = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(lm, o) : fminf(lm, o);
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const float o = __shfl_xor_sync(FULL, lm, j);
+          lm = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(lm, o) : fminf(lm, o);
+        }
+      const float t0 = __shfl_sync(FULL, lm, Meff - 1);
+      m0 = __shfl_sync(FULL, lm, 0);
+      if (t0 != -INFINITY) {
+        c.theta = (uint64_t)ord_f32(t0) << 32;  // (t0, token = +inf): x == t0 still passes
+        c.theta_x = t0;
       }
-    const float t0 = __shfl_sync(FULL, lm, Meff - 1);
-    const float m0 = __shfl_sync(FULL, lm, 0);
+    }
     if (m0 > M_FLOOR) {
       m = m0;
       m_thr = m0 + RESCALE_MARGIN;
       nml2 = pk2(-m * VS_LOG2E, -m * VS_LOG2E);
     }
-    if (t0 != -INFINITY) {
-      c.theta = (uint64_t)ord_f32(t0) << 32;  // (t0, token = +inf): x == t0 still passes
-      c.theta_x = t0;
-    }
+  };
+  // lane max with its first token over one vector (bootstrap only)
+  auto lane_argmax = [&](const float (&x)[VEC], int tok0, float& lm, int& lt) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j)
+      if (x[j] > lm) {
+        lm = x[j];
+        lt = tok0 + j;
+      }
   };
 
   if (active) {
@@ -463,6 +534,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         for (int ch = 0; ch < min(NS, nch); ++ch) issue(ch);
       if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 chunks
         float lm = -INFINITY;
+        int lt = 0;
         for (int ch = 0; ch < min(2, nch); ++ch) {
           tk::mbar_wait(&bars[ch], 0);
           const uint4* sv = stg + ch * CH;
@@ -472,12 +544,11 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
             if (ch * CH + i < nvt) {
               float x[VEC];
               unpack<T>(sv[i], x);
-#pragma unroll
-              for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+              lane_argmax(x, (v0 + ch * CH + i) * VEC, lm, lt);
             }
           }
         }
-        boot(lm);
+        boot(lm, lt);
       }
       for (int ch = 0; ch < nch; ++ch) {
         const int q = ch % NS;
@@ -523,21 +594,24 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
       }
       if (Meff <= 32) {  // bootstrap θ: M-th largest of 32 lane maxima over 2 batches
         float lm = -INFINITY;
+        int lt = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           float x[VEC];
           if (v0 + lane + 32 * u < v1) {
             unpack<T>(cur[u], x);
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
-          }
-          if (v0 + BATCH + lane + 32 * u < v1) {
-            unpack<T>(nxt[u], x);
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) lm = fmaxf(lm, x[j]);
+            lane_argmax(x, (v0 + lane + 32 * u) * VEC, lm, lt);
           }
         }
-        boot(lm);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float x[VEC];
+          if (v0 + BATCH + lane + 32 * u < v1) {
+            unpack<T>(nxt[u], x);
+            lane_argmax(x, (v0 + BATCH + lane + 32 * u) * VEC, lm, lt);
+          }
+        }
+        boot(lm, lt);
       }
       int base = v0;
       const int pf_dist = 2 * BATCH * pf_batches;  // vectors ahead of the demand loads
@@ -602,9 +676,11 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     }
   }
   if (TL) {  // hand the list to the common epilogue as a sorted buffer
-    const bool has = lane < Meff && tl.tk != 0ull;
-    if (has) buf[lane] = tl.tk;
+    const bool has = lane < Meff && tl.tk != (K)0;
+    if (has) buf[lane] = KeyOps<K>::to64(tl.tk);
     c.cnt = __popc(__ballot_sync(FULL, has));
+    c.theta = KeyOps<K>::to64(tl.theta);
+    c.theta_x = tl.theta_x;
     __syncwarp();
   }
   // ---- per-warp lse partial -> exchange --------------------------------------------
@@ -724,7 +800,7 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   static int variant = -1, flush_min = FLUSH_MIN, pf = 0;  // knobs: VS_K1_VARIANT/_FLUSH/_PF/_C0
-  static int tl_mode = 1;                                   // VS_K1_TL=0: buffered candidates
+  static int tl_mode = 1;  // VS_K1_TL: 0 buffered candidates, 3 top-list with 64-bit keys only
   static float c0 = PICKW_C0;
   if (variant < 0) {
     const char* y = getenv("VS_K1_TL");
@@ -758,7 +834,8 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     grid = (rows * pick_w(rows, V, Tw, c0) + WPC - 1) / WPC;
   }
   const T* p = static_cast<const T*>(logits);
-  const bool TLm = (M < V ? M : V) <= 32 && tl_mode;
+  // candidate mode: register top-list for Meff <= 32, 32-bit keys for bf16 rows with |V| < 65536
+  const int TLm = ((M < V ? M : V) <= 32 && tl_mode) ? ((sizeof(T) == 2 && V < 65536 && tl_mode != 3) ? 2 : 1) : 0;
 #define VS_K1_LAUNCH(U_, B_, TL_, NS_)                                                                  \
   do {                                                                                                   \
     auto kern = row_lse_topm_warp_kernel<T, U_, B_, TL_, NS_>;                                           \
@@ -767,11 +844,13 @@ int launch(const void* logits, int64_t ld, int V, int M, int R_host, const int* 
     vs::vs_launch(kern, dim3(grid), dim3(WPC * 32), dsm, st, p, ld, V, M, R_host, d_R, top_tok, top_logp,    \
                   row_lse, fb, norm, sms, flush_min, pf, ctas_per_sm * WPC, c0);                         \
   } while (0)
-#define VS_K1_LAUNCH3(U_, B_, NS_)     \
-  if (TLm)                             \
-    VS_K1_LAUNCH(U_, B_, true, NS_);   \
-  else                                 \
-    VS_K1_LAUNCH(U_, B_, false, NS_);
+#define VS_K1_LAUNCH3(U_, B_, NS_)  \
+  if (TLm == 2)                     \
+    VS_K1_LAUNCH(U_, B_, 2, NS_);   \
+  else if (TLm == 1)                \
+    VS_K1_LAUNCH(U_, B_, 1, NS_);   \
+  else                              \
+    VS_K1_LAUNCH(U_, B_, 0, NS_);
   switch (variant) {
     case 0: VS_K1_LAUNCH3(4, 2, 0); break;
     case 3: VS_K1_LAUNCH3(3, 3, 0); break;
