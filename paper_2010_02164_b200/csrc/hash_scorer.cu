@@ -29,13 +29,13 @@ __global__ void hash_encode_kernel(vs_config cfg, vs_state st, uint64_t seed) {
 __device__ __forceinline__ float hash_logit(uint32_t key, int v, float scale, int power) {
   const uint32_t bits = fmix32(((uint32_t)v * 0x9E3779B9u) ^ key);
   if (power == 0) {  // log-like: -scale * (e + f), u' = ((bits>>8)+1) * 2^-24 = 2^e (1+f)
-    const float u1 = __fmul_rn((float)((bits >> 8) + 1u), 5.9604644775390625e-08f);
-    const uint32_t ub = __float_as_uint(u1);
-    // e and f without int->float conversions (XU pipe): both are exact —
-    // e via the 1.5*2^23 shifter, f = (1 + m*2^-23) - 1 (Sterbenz).
-    const float e = __fsub_rn(__int_as_float(0x4B400000 + (int)(ub >> 23) - 127), 12582912.0f);
-    const float f = __fsub_rn(__uint_as_float(0x3F800000u | (ub & 0x7FFFFFu)), 1.0f);
-    return __fmul_rn(-scale, __fadd_rn(e, f));
+    // e + f = (bits(u') - bits(1.0)) * 2^-23 exactly up to one rounding, and
+    // bits(u') = bits(float(n)) - 24·2^23, so the logit is two conversions, an
+    // add and two multiplies (bit-identical to the oracle's e/f formula: float
+    // rounding commutes with the power-of-two scalings).
+    const uint32_t n = (bits >> 8) + 1u;
+    const int X = (int)(__float_as_uint((float)n) - 0x4B800000u);
+    return __fmul_rn(__fmul_rn((float)X, 1.1920928955078125e-07f), -scale);
   }
   float u = __fmul_rn((float)(bits >> 8), 5.9604644775390625e-08f);  // * 2^-24, exact
   if (power >= 2) u = __fmul_rn(u, u);
@@ -70,11 +70,15 @@ __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_stat
         __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
     T* out = logits + (int64_t)r * ld;
     T vals[8];
+    if ((unsigned)(cfg.eos - v0) < 8u) {  // the one chunk holding EOS
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int v = v0 + j;
-      const float x = (v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power);
-      vals[j] = cvt<T>(x);
+      for (int j = 0; j < 8; ++j) {
+        const int v = v0 + j;
+        vals[j] = cvt<T>((v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) vals[j] = cvt<T>(hash_logit(key, v0 + j, hp.scale, hp.power));
     }
     const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
     if (vec_ok) {
