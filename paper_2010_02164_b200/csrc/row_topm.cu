@@ -350,10 +350,10 @@ __device__ __forceinline__ float tl_seed(TopList<K>& t, float lm, int lt, int Me
 __host__ __device__ __forceinline__ int pick_w(int R, int V, int T, float c0 = PICKW_C0) {
   if (V < 4096 || R <= 0) return 1;
   int best = 1;
-  float bc = 1e30f;
-  for (int w = 1; w <= WPC; w <<= 1) {
-    const float waves = (float)(((long)R * w + T - 1) / T);
-    const float cost = waves * (c0 + 1.0f / w);
+  float bc = 1e30f, inv = 1.0f;  // 32-bit unsigned math: this runs in every warp's prologue
+  for (int w = 1; w <= WPC; w <<= 1, inv *= 0.5f) {
+    const float waves = (float)(((unsigned)R * (unsigned)w + (unsigned)T - 1u) / (unsigned)T);
+    const float cost = waves * (c0 + inv);
     if (cost < bc - 1e-6f) {
       bc = cost;
       best = w;
@@ -690,12 +690,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     up2(s01, a, b);
     s = a + b;
   }
+  // m is warp-uniform (RESCALE_MARGIN), so the warp's partial sums add directly
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(FULL, m, o);
-    const float s2 = __shfl_xor_sync(FULL, s, o);
-    lse_merge(m, s, m2, s2);
-  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
   if (W > 1) {
     if (lane == 0) {
       spart[wid].m = m;

@@ -11,7 +11,8 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -shared -Xcompiler -
   -DK1_ABL_NOCAND -DK1_ABL_NOEXP -o ../_lib/abl_BOTH.so *.cu 2>/dev/null
 wait
 cd ../..
+R=${1:-6400}
 for l in libvarstream abl_NOCAND abl_NOEXP abl_BOTH; do
-  echo -n "$l :: "; VARSTREAM_LIB=paper_2010_02164_b200/_lib/$l.so timeout 100 python tools/prof_k1.py 6400 42024 5 --legacy | tail -1
+  echo -n "$l :: "; VARSTREAM_LIB=paper_2010_02164_b200/_lib/$l.so timeout 100 python tools/prof_k1.py $R 42024 5 --legacy | tail -1
 done
 rm -f paper_2010_02164_b200/_lib/abl_*.so

@@ -1,6 +1,6 @@
 """Standalone K1 timing / ncu driver: R rows x |V| logits (log-like values).
 
-    python tools/prof_k1.py [R] [V] [M] [f32|bf16] [--noflush] [--legacy]
+    python tools/prof_k1.py [R] [V] [M] [f32|bf16] [--noflush] [--legacy] [--b2b]
 
 Outputs are pre-allocated and K1 is launched through the C-ABI directly, so
 the CUDA events bracket only the kernel (an L2-flush kernel runs before each
@@ -51,6 +51,19 @@ def launch():
                                        ws.numel(), stream), "k1")
 
 
+if "--b2b" in sys.argv:  # back-to-back launches (inputs > L2), no flush, no host gaps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(12)]
+    launch()
+    for e0, e1 in evs:
+        e0.record()
+        launch()
+        e1.record()
+    torch.cuda.synchronize()
+    ts = sorted(e0.elapsed_time(e1) for e0, e1 in evs)
+    med = ts[len(ts) // 2]
+    print("K1 b2b ms per launch (sorted):", [round(t, 4) for t in ts], "GB/s:",
+          round(R * V * x.element_size() / med / 1e6, 1), "fallbacks:", int(fb.item()))
+    sys.exit(0)
 ts = []
 for i in range(8):
     if flush_between:
