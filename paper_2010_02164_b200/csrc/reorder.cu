@@ -13,27 +13,38 @@
 namespace vs {
 namespace {
 
+// Persistent grid: CTAs stride over the (copy, plane) items of the device-side
+// n_copy; each item is copied with 4 independent 16-byte loads in flight per
+// thread before their stores (the row of one item is up to max_len·pos_bytes).
 __global__ void __launch_bounds__(256) rows_copy_kernel(unsigned char* __restrict__ base,
                                                         int64_t plane_stride, int planes,
                                                         int64_t row_stride, int64_t pos_bytes,
                                                         const int32_t* __restrict__ copy_list,
                                                         const int32_t* __restrict__ n_copy) {
   VS_PDL_ENTRY();
-  const int c = blockIdx.x;
-  if (c >= *n_copy) return;
-  const int plane = blockIdx.y;
-  if (plane >= planes) return;
-  const int src = copy_list[3 * c], dst = copy_list[3 * c + 1], len = copy_list[3 * c + 2];
-  const int64_t bytes = (int64_t)len * pos_bytes;
-  const unsigned char* s = base + plane * plane_stride + (int64_t)src * row_stride;
-  unsigned char* d = base + plane * plane_stride + (int64_t)dst * row_stride;
-  if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes) & 15) == 0) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(s);
-    uint4* d4 = reinterpret_cast<uint4*>(d);
-    const int64_t n4 = bytes >> 4;
-    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) d4[i] = s4[i];
-  } else {
-    for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) d[i] = s[i];
+  const int items = *n_copy * planes;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int c = it / planes, plane = it - c * planes;
+    const int src = copy_list[3 * c], dst = copy_list[3 * c + 1], len = copy_list[3 * c + 2];
+    const int64_t bytes = (int64_t)len * pos_bytes;
+    const unsigned char* s = base + plane * plane_stride + (int64_t)src * row_stride;
+    unsigned char* d = base + plane * plane_stride + (int64_t)dst * row_stride;
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes) & 15) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(s);
+      uint4* d4 = reinterpret_cast<uint4*>(d);
+      const int64_t n4 = bytes >> 4;
+      int64_t i = threadIdx.x;
+      for (; i + 3 * 256 < n4; i += 4 * 256) {
+        const uint4 v0 = s4[i], v1 = s4[i + 256], v2 = s4[i + 512], v3 = s4[i + 768];
+        d4[i] = v0;
+        d4[i + 256] = v1;
+        d4[i + 512] = v2;
+        d4[i + 768] = v3;
+      }
+      for (; i < n4; i += 256) d4[i] = s4[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) d[i] = s[i];
+    }
   }
 }
 
@@ -66,7 +77,14 @@ extern "C" int vs_rows_copy(void* base, int64_t plane_stride_bytes, int32_t plan
   if (!base || !copy_list || !n_copy || planes < 1 || planes > 65535 || pos_bytes < 1)
     return VS_ERR_CONFIG;
   if (max_copies <= 0) return VS_OK;
-  dim3 grid(max_copies, planes);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long need = (long)max_copies * planes;
+  const int grid = (int)(need < (long)sms * 8 ? need : (long)sms * 8);
   vs::vs_launch(vs::rows_copy_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<unsigned char*>(base), plane_stride_bytes, planes, row_stride_bytes, pos_bytes,
       copy_list, n_copy);
