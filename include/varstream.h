@@ -250,6 +250,17 @@ int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void* v_cache, 
                      int32_t head_dim, float scale, int32_t R_host, const int32_t* d_R, int32_t R_grid,
                      void* stream);
 
+/* Grouped decode attention (no append) for rows that share one cache row:
+ * group g (g < *d_ngroups, G_grid bounds it) is rows [grp_off[g], grp_off[g+1]),
+ * all with the same idx and lens (the cross-attention of one beam: grp_off =
+ * the engine's sel_off, *d_ngroups = status[VS_ST_NSEL]).  One CTA per
+ * (group, head) stages the shared K/V lines in shared memory once; per row the
+ * result is bit-identical to vs_row_attention.  head_dim 64, lens <= 256. */
+int vs_row_attention_grouped(const void* q, int64_t q_ld, const void* k_cache, const void* v_cache,
+                             int64_t row_stride, int64_t pos_stride, const int32_t* idx, const int32_t* lens,
+                             const int32_t* grp_off, const int32_t* d_ngroups, int32_t G_grid, void* out,
+                             int64_t out_ld, int32_t heads, int32_t head_dim, float scale, void* stream);
+
 /* K5  proj_lse_topM — the decoder's vocab projection on tcgen05 tensor cores
  * with K1 fused into the epilogue (csrc/proj_topm.cu).  For rows r < R
  * (R = *d_R when d_R != NULL, else R_host; R_grid bounds R and sizes the TMA

@@ -63,7 +63,7 @@ class VsHashParams(C.Structure):
 
 # Every symbol include/varstream.h declares (checked by tests/test_native_exports.py).
 EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step", "vs_schedule", "vs_rows_copy",
-           "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention",
+           "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention", "vs_row_attention_grouped",
            "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes")
 
 _lib = None
@@ -95,6 +95,8 @@ def load_library(path: Path | None = None) -> C.CDLL:
         "vs_proj_lse_topm_ws_bytes": ([i32, i32], C.c_size_t),
         "vs_row_attention": ([vp, i64, vp, vp, i64, i64, vp, vp, vp, vp, i64, vp, i64, i32, i32, C.c_float,
                               i32, vp, i32, vp], i32),
+        "vs_row_attention_grouped": ([vp, i64, vp, vp, i64, i64, vp, vp, vp, vp, i32, vp, i64, i32, i32,
+                                      C.c_float, vp], i32),
         "vs_hash_logits": ([C.POINTER(VsConfig), C.POINTER(VsState), C.POINTER(VsHashParams), vp,
                             i64, i32, vp], i32),
     }

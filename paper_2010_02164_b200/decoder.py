@@ -306,6 +306,17 @@ class GraphedTransformerScorer(TransformerScorer):
             out.data_ptr(), out.stride(0), self.h, 64, 1.0 / 8.0, R, None, R,
             torch.cuda.current_stream(self.device).cuda_stream), "vs_row_attention")
 
+    def _row_attn_grouped(self, q, kc, vc, idx, lens, out):
+        """Cross-attention: the rows of one selected beam share the slot's encoder
+        states (groups = engine sel_off / status NSEL; padded rows are not in any
+        group and keep their self-attention output, finite and unused)."""
+        eng = self.engine
+        N.check(eng.lib.vs_row_attention_grouped(
+            q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), kc.stride(0), kc.stride(1),
+            idx.data_ptr(), lens.data_ptr(), eng.t["sel_off"].data_ptr(), eng.status_ptr(N.ST_NSEL), eng.n,
+            out.data_ptr(), out.stride(0), self.h, 64, 1.0 / 8.0,
+            torch.cuda.current_stream(self.device).cuda_stream), "vs_row_attention_grouped")
+
     def _body(self, Rb: int):
         eng, t, d = self.engine, self.engine.t, self.d
         Lmax = eng.max_len
@@ -326,7 +337,7 @@ class GraphedTransformerScorer(TransformerScorer):
                        qkv[:, 2 * d:], att)
             x = F.layer_norm(x + att @ L["o"].T, (d,))
             cq = x @ L["cq"].T
-            self._row_attn(cq, self.enc_kv[li, 0], self.enc_kv[li, 1], slot, enc_len, None, None, att)
+            self._row_attn_grouped(cq, self.enc_kv[li, 0], self.enc_kv[li, 1], slot, enc_len, att)
             x = F.layer_norm(x + att @ L["co"].T, (d,))
             x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (d,))
         lg = self.lg[:Rb, : self.vocab.size]

@@ -581,3 +581,66 @@ def test_sharded_concurrent_run_gathers_single_run_outputs(tmp_path):
     want, _ = P.run_varstream(corpus, sc, cfg)
     got = pickle.loads(out.read_bytes())
     assert got == [[(c.tokens, c.score) for c in per] for per in want]
+
+
+@pytest.mark.parametrize("append", [False, True])
+def test_row_attention_matches_torch_and_grouped_is_bit_identical(append):
+    """vs_row_attention (in-place decode attention over cache rows, optional
+    append of the newest position) vs a torch fp32 softmax attention; the
+    grouped cross-attention kernel (shared cache row per group, K/V staged in
+    shared memory) gives bit-identical rows."""
+    P, N, *_ = _pkg()
+    lib = N.load_library()
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(7)
+    H, D, nrow, Lmax = 8, 64, 6, 256
+    lens_g = [1, 5, 33, 64, 200, 256]  # per cache row
+    groups = [(0, 3), (1, 2), (2, 7), (3, 1), (4, 4), (5, 2)]  # (cache row, rows in group)
+    idx = torch.tensor([c for c, n_ in groups for _ in range(n_)], dtype=torch.int32, device=dev)
+    lens = torch.tensor([lens_g[c] for c, n_ in groups for _ in range(n_)], dtype=torch.int32, device=dev)
+    R = idx.numel()
+    kc = torch.randn(nrow, Lmax, H * D, generator=g, device=dev).to(torch.bfloat16)
+    vc = torch.randn(nrow, Lmax, H * D, generator=g, device=dev).to(torch.bfloat16)
+    q = torch.randn(R, H * D, generator=g, device=dev).to(torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    out = torch.empty(R, H * D, dtype=torch.bfloat16, device=dev)
+    if append:  # one private cache row per query row, newest position from k_new/v_new
+        rows = torch.arange(R, dtype=torch.int32, device=dev)
+        kc2 = kc[idx.long()].clone()
+        vc2 = vc[idx.long()].clone()
+        kn = torch.randn(R, H * D, generator=g, device=dev).to(torch.bfloat16)
+        vn = torch.randn(R, H * D, generator=g, device=dev).to(torch.bfloat16)
+        N.check(lib.vs_row_attention(q.data_ptr(), q.stride(0), kc2.data_ptr(), vc2.data_ptr(), kc2.stride(0),
+                                     kc2.stride(1), rows.data_ptr(), lens.data_ptr(), kn.data_ptr(), vn.data_ptr(),
+                                     kn.stride(0), out.data_ptr(), out.stride(0), H, D, 0.125, R, None, R, st),
+                "attn")
+        ar = torch.arange(R, device=dev)
+        assert torch.equal(kc2[ar, lens.long() - 1], kn) and torch.equal(vc2[ar, lens.long() - 1], vn)
+        K, Vv = kc2, vc2
+        crow = ar
+    else:
+        N.check(lib.vs_row_attention(q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), kc.stride(0),
+                                     kc.stride(1), idx.data_ptr(), lens.data_ptr(), None, None, 0, out.data_ptr(),
+                                     out.stride(0), H, D, 0.125, R, None, R, st), "attn")
+        K, Vv = kc, vc
+        crow = idx.long()
+    torch.cuda.synchronize()
+    for r in range(R):
+        L = int(lens[r])
+        qq = q[r].float().view(H, D)
+        kk = K[crow[r], :L].float().view(L, H, D)
+        vv = Vv[crow[r], :L].float().view(L, H, D)
+        p = torch.softmax(torch.einsum("hd,lhd->hl", qq, kk) * 0.125, dim=-1)
+        ref = torch.einsum("hl,lhd->hd", p, vv).reshape(-1)
+        assert torch.allclose(out[r].float(), ref, atol=2e-2, rtol=2e-2), f"row {r}"
+    if not append:
+        off = torch.tensor(np.concatenate([[0], np.cumsum([n_ for _, n_ in groups])]), dtype=torch.int32,
+                           device=dev)
+        ng = torch.tensor([len(groups)], dtype=torch.int32, device=dev)
+        out2 = torch.full_like(out, float("nan"))
+        N.check(lib.vs_row_attention_grouped(q.data_ptr(), q.stride(0), kc.data_ptr(), vc.data_ptr(), kc.stride(0),
+                                             kc.stride(1), idx.data_ptr(), lens.data_ptr(), off.data_ptr(),
+                                             ng.data_ptr(), len(groups) + 2, out2.data_ptr(), out2.stride(0), H, D,
+                                             0.125, st), "attn_grouped")
+        torch.cuda.synchronize()
+        assert torch.equal(out2, out)
