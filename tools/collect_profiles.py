@@ -17,7 +17,7 @@ src = ROOT / "gpurun_out"
 dst = ROOT / "profiles" / rnd
 dst.mkdir(parents=True, exist_ok=True)
 summary = {}
-for rep in ("k1_fullwidth", "k1_decode", "step_kernels", "k1t_fw", "k1t_573", "k5_1300"):
+for rep in ("k1_fullwidth", "k1_decode", "step_kernels", "k1t_fw", "k1t_573", "k5_1300", "dec_attention"):
     p = src / f"{rep}.ncu-rep"
     if not p.exists():
         continue

@@ -19,4 +19,6 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:proj
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"beam_step|schedule|hash_logits" -s 1200 -c 3 \
     -o gpurun_out/step_kernels python bench.py --no-cpu-baseline --steps 1 --warmup 3 --e2e-steps 1 --n-inputs 2000 --decoder-inputs 0 > /dev/null 2>&1
 timeout 600 bash tools/decoder_launches.sh > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:row_attention -s 600 -c 2 \
+    -o gpurun_out/dec_attention python tools/decoder_probe.py 300 4 12 > /dev/null 2>&1
 ls -la gpurun_out
