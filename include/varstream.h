@@ -254,8 +254,9 @@ int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void* v_cache, 
  * group g (g < *d_ngroups, G_grid bounds it) is rows [grp_off[g], grp_off[g+1]),
  * all with the same idx and lens (the cross-attention of one beam: grp_off =
  * the engine's sel_off, *d_ngroups = status[VS_ST_NSEL]).  One CTA per
- * (group, head) stages the shared K/V lines in shared memory once; per row the
- * result is bit-identical to vs_row_attention.  head_dim 64, lens <= 256. */
+ * (group, head) stages the shared K/V lines (and 64 query rows at a time) in
+ * shared memory once and runs mma.m16n8k16 tiles with an online softmax (P in
+ * bf16, fp32 accumulation).  head_dim 64, lens <= 256. */
 int vs_row_attention_grouped(const void* q, int64_t q_ld, const void* k_cache, const void* v_cache,
                              int64_t row_stride, int64_t pos_stride, const int32_t* idx, const int32_t* lens,
                              const int32_t* grp_off, const int32_t* d_ngroups, int32_t G_grid, void* out,

@@ -181,41 +181,176 @@ __global__ void __launch_bounds__(HPC * 32, 6) row_attention_kernel(
 }
 
 // Grouped rows sharing one cache row (cross-attention: a beam's rows all read
-// their slot's encoder states).  One CTA per (group, head): the slot's K/V
-// lines of that head are staged once into shared memory (chunk c of position t
-// at c ^ (t & 7): conflict-free 16-byte reads for lanes over positions), then
-// the CTA's warps take the group's rows.  Per row the arithmetic is the one of
-// row_attention_kernel, so the outputs are bit-identical to it.
-constexpr int GW = 8;
-__global__ void __launch_bounds__(GW * 32) row_attention_grouped_kernel(
+// their slot's encoder states) on the tensor cores.  One CTA (4 warps) per
+// (group, head): the slot's K/V lines of that head (<= 256 positions) and up to
+// 64 of the group's query rows are staged in shared memory (16-byte chunks
+// XOR-swizzled by row for conflict-free ldmatrix), and each warp runs a
+// FlashAttention-2 style pass for 16 rows: S = Q·K^T with mma.m16n8k16 (bf16
+// in, fp32 accumulate) over 64-position tiles, online softmax in fp32, P
+// (bf16) · V with mma.  Per beam the K/V tile is read once for all its rows.
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+               "{%8, %9}, {%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int GROWS = 64;  // query rows per CTA pass (4 warps x 16)
+__global__ void __launch_bounds__(128) row_attention_grouped_kernel(
     const __nv_bfloat16* __restrict__ q, int64_t q_ld, const __nv_bfloat16* __restrict__ kc,
     const __nv_bfloat16* __restrict__ vc, int64_t row_stride, int64_t pos_stride, const int* __restrict__ idx,
     const int* __restrict__ lens, const int* __restrict__ grp_off, const int* __restrict__ d_ngrp,
     __nv_bfloat16* __restrict__ out, int64_t out_ld, float scale) {
   VS_PDL_ENTRY();
-  extern __shared__ __align__(16) uint4 kvs[];  // [2][MAXL][8] 16-byte chunks
-  __shared__ float sp[GW][MAXL];
+  extern __shared__ __align__(128) uint4 sm[];
+  uint4* Ks = sm;                  // [MAXL][8]
+  uint4* Vs = sm + MAXL * 8;       // [MAXL][8]
+  uint4* Qs = sm + 2 * MAXL * 8;   // [GROWS][8]
   const int gi = blockIdx.x;
   if (gi >= *d_ngrp) return;
   const int r0 = grp_off[gi], nr = grp_off[gi + 1] - r0;
   if (nr <= 0) return;
-  const int h = blockIdx.y;
-  const int64_t hoff = (int64_t)h * DH;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t hoff = (int64_t)blockIdx.y * DH;
   const int L = lens[r0];
   const int64_t row = idx[r0];
-  uint4* ks = kvs;
-  uint4* vs = kvs + MAXL * 8;
-  for (int i = threadIdx.x; i < L * 8; i += GW * 32) {
+  const int Lt = (L + 63) & ~63;
+  for (int i = tid; i < Lt * 8; i += 128) {  // K/V lines of this (slot, head); zero past L
     const int t = i >> 3, c = i & 7;
-    const int64_t off = row * row_stride + (int64_t)t * pos_stride + hoff;
-    ks[t * 8 + (c ^ (t & 7))] = reinterpret_cast<const uint4*>(kc + off)[c];
-    vs[t * 8 + (c ^ (t & 7))] = reinterpret_cast<const uint4*>(vc + off)[c];
+    uint4 kv = make_uint4(0u, 0u, 0u, 0u), vv = kv;
+    if (t < L) {
+      const int64_t off = row * row_stride + (int64_t)t * pos_stride + hoff;
+      kv = reinterpret_cast<const uint4*>(kc + off)[c];
+      vv = reinterpret_cast<const uint4*>(vc + off)[c];
+    }
+    Ks[t * 8 + (c ^ (t & 7))] = kv;
+    Vs[t * 8 + (c ^ (t & 7))] = vv;
   }
-  __syncthreads();
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto kline = [&](int t, int c) -> uint4 { return ks[t * 8 + (c ^ (t & 7))]; };
-  auto vline = [&](int t, int c) -> uint4 { return vs[t * 8 + (c ^ (t & 7))]; };
-  for (int rr = wid; rr < nr; rr += GW) attend(q, q_ld, r0 + rr, hoff, L, scale, lane, sp[wid], kline, vline, out, out_ld);
+  const float sl2 = scale * 1.4426950408889634f;  // softmax in base 2
+  for (int c0 = 0; c0 < nr; c0 += GROWS) {
+    const int n = min(GROWS, nr - c0);
+    for (int i = tid; i < GROWS * 8; i += 128) {
+      const int rr = i >> 3, c = i & 7;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (rr < n) v = reinterpret_cast<const uint4*>(q + (int64_t)(r0 + c0 + rr) * q_ld + hoff)[c];
+      Qs[rr * 8 + (c ^ (rr & 7))] = v;
+    }
+    __syncthreads();
+    if (16 * w < n) {
+      const int mi = lane >> 3, li = lane & 7;
+      uint32_t a[4][4];  // Q fragments, 4 k16 steps over the 64 dims
+#pragma unroll
+      for (int k16 = 0; k16 < 4; ++k16) {
+        const int rr = 16 * w + li + ((mi & 1) ? 8 : 0), c = 2 * k16 + (mi >> 1);
+        ldsm_x4(a[k16], smem_addr(Qs + rr * 8 + (c ^ (rr & 7))));
+      }
+      float o[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+      float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;  // rows lane/4 and lane/4 + 8
+      for (int p0 = 0; p0 < Lt; p0 += 64) {
+        float sc[8][4];
+#pragma unroll
+        for (int n8 = 0; n8 < 8; ++n8) {
+          sc[n8][0] = sc[n8][1] = sc[n8][2] = sc[n8][3] = 0.f;
+          const int pos = p0 + 8 * n8 + li;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            uint32_t b[4];
+            const int c = 4 * kk + mi;
+            ldsm_x4(b, smem_addr(Ks + pos * 8 + (c ^ (pos & 7))));
+            mma_bf16(sc[n8], a[2 * kk], b[0], b[1]);
+            mma_bf16(sc[n8], a[2 * kk + 1], b[2], b[3]);
+          }
+        }
+        float mx_a = -INFINITY, mx_b = -INFINITY;
+#pragma unroll
+        for (int n8 = 0; n8 < 8; ++n8)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int pos = p0 + 8 * n8 + 2 * (lane & 3) + (e & 1);
+            const float v = pos < L ? sc[n8][e] * sl2 : -INFINITY;
+            sc[n8][e] = v;
+            if (e < 2) mx_a = fmaxf(mx_a, v);
+            else mx_b = fmaxf(mx_b, v);
+          }
+#pragma unroll
+        for (int o2 = 1; o2 <= 2; o2 <<= 1) {
+          mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, o2));
+          mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, o2));
+        }
+        const float mn_a = fmaxf(m_a, mx_a), mn_b = fmaxf(m_b, mx_b);
+        const float cr_a = m_a == -INFINITY ? 0.f : exp2f(m_a - mn_a);  // 0 on the first tile
+        const float cr_b = m_b == -INFINITY ? 0.f : exp2f(m_b - mn_b);
+        m_a = mn_a;
+        m_b = mn_b;
+        l_a *= cr_a;
+        l_b *= cr_b;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o[j][0] *= cr_a;
+          o[j][1] *= cr_a;
+          o[j][2] *= cr_b;
+          o[j][3] *= cr_b;
+        }
+        uint32_t pa[4][4];  // P as A fragments, 4 k16 steps over the tile's 64 positions
+#pragma unroll
+        for (int n8 = 0; n8 < 8; ++n8) {
+          const float p0v = exp2f(sc[n8][0] - mn_a), p1v = exp2f(sc[n8][1] - mn_a);
+          const float p2v = exp2f(sc[n8][2] - mn_b), p3v = exp2f(sc[n8][3] - mn_b);
+          l_a += p0v + p1v;
+          l_b += p2v + p3v;
+          pa[n8 >> 1][(n8 & 1) * 2] = pack_bf16(p0v, p1v);
+          pa[n8 >> 1][(n8 & 1) * 2 + 1] = pack_bf16(p2v, p3v);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int pos = p0 + 16 * t + li + ((mi & 1) ? 8 : 0);
+#pragma unroll
+          for (int n8 = 0; n8 < 8; n8 += 2) {
+            uint32_t b[4];
+            const int c = n8 + (mi >> 1);
+            ldsm_x4_t(b, smem_addr(Vs + pos * 8 + (c ^ (pos & 7))));
+            mma_bf16(o[n8], pa[t], b[0], b[1]);
+            mma_bf16(o[n8 + 1], pa[t], b[2], b[3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int o2 = 1; o2 <= 2; o2 <<= 1) {
+        l_a += __shfl_xor_sync(0xffffffffu, l_a, o2);
+        l_b += __shfl_xor_sync(0xffffffffu, l_b, o2);
+      }
+      const float ia = l_a > 0.f ? 1.f / l_a : 0.f, ib = l_b > 0.f ? 1.f / l_b : 0.f;
+      const int ra = 16 * w + (lane >> 2), rb = ra + 8;
+#pragma unroll
+      for (int n8 = 0; n8 < 8; ++n8) {
+        const int d = 8 * n8 + 2 * (lane & 3);
+        if (ra < n)
+          *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + c0 + ra) * out_ld + hoff + d) =
+              pack_bf16(o[n8][0] * ia, o[n8][1] * ia);
+        if (rb < n)
+          *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + c0 + rb) * out_ld + hoff + d) =
+              pack_bf16(o[n8][2] * ib, o[n8][3] * ib);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -248,12 +383,12 @@ extern "C" int vs_row_attention_grouped(const void* q, int64_t q_ld, const void*
     return VS_ERR_CONFIG;
   if (G_grid == 0) return VS_OK;
   static bool attr = false;
-  const size_t dsm = 2 * vs::MAXL * 8 * sizeof(uint4);  // 64 KB: K and V of one (slot, head)
+  const size_t dsm = (2 * vs::MAXL + vs::GROWS) * 8 * sizeof(uint4);  // K, V of one (slot, head) + Q rows
   if (!attr) {
     cudaFuncSetAttribute(vs::row_attention_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
     attr = true;
   }
-  vs::vs_launch(vs::row_attention_grouped_kernel, dim3(G_grid, heads), dim3(32 * vs::GW), dsm,
+  vs::vs_launch(vs::row_attention_grouped_kernel, dim3(G_grid, heads), dim3(128), dsm,
                 static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(q), q_ld,
                 static_cast<const __nv_bfloat16*>(k_cache), static_cast<const __nv_bfloat16*>(v_cache), row_stride,
                 pos_stride, idx, lens, grp_off, d_ngroups, static_cast<__nv_bfloat16*>(out), out_ld, scale);

@@ -584,18 +584,18 @@ def test_sharded_concurrent_run_gathers_single_run_outputs(tmp_path):
 
 
 @pytest.mark.parametrize("append", [False, True])
-def test_row_attention_matches_torch_and_grouped_is_bit_identical(append):
+def test_row_attention_matches_torch(append):
     """vs_row_attention (in-place decode attention over cache rows, optional
-    append of the newest position) vs a torch fp32 softmax attention; the
-    grouped cross-attention kernel (shared cache row per group, K/V staged in
-    shared memory) gives bit-identical rows."""
+    append of the newest position) and vs_row_attention_grouped (rows sharing a
+    cache row, tensor-core tiles; groups of 1..70 rows, 1..256 positions) vs a
+    torch fp32 softmax attention."""
     P, N, *_ = _pkg()
     lib = N.load_library()
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(7)
     H, D, nrow, Lmax = 8, 64, 6, 256
     lens_g = [1, 5, 33, 64, 200, 256]  # per cache row
-    groups = [(0, 3), (1, 2), (2, 7), (3, 1), (4, 4), (5, 2)]  # (cache row, rows in group)
+    groups = [(0, 3), (1, 2), (2, 7), (3, 1), (4, 70), (5, 2)]  # (cache row, rows in group)
     idx = torch.tensor([c for c, n_ in groups for _ in range(n_)], dtype=torch.int32, device=dev)
     lens = torch.tensor([lens_g[c] for c, n_ in groups for _ in range(n_)], dtype=torch.int32, device=dev)
     R = idx.numel()
@@ -625,14 +625,15 @@ def test_row_attention_matches_torch_and_grouped_is_bit_identical(append):
         K, Vv = kc, vc
         crow = idx.long()
     torch.cuda.synchronize()
+    refs = []
     for r in range(R):
         L = int(lens[r])
         qq = q[r].float().view(H, D)
         kk = K[crow[r], :L].float().view(L, H, D)
         vv = Vv[crow[r], :L].float().view(L, H, D)
         p = torch.softmax(torch.einsum("hd,lhd->hl", qq, kk) * 0.125, dim=-1)
-        ref = torch.einsum("hl,lhd->hd", p, vv).reshape(-1)
-        assert torch.allclose(out[r].float(), ref, atol=2e-2, rtol=2e-2), f"row {r}"
+        refs.append(torch.einsum("hl,lhd->hd", p, vv).reshape(-1))
+        assert torch.allclose(out[r].float(), refs[-1], atol=2e-2, rtol=2e-2), f"row {r}"
     if not append:
         off = torch.tensor(np.concatenate([[0], np.cumsum([n_ for _, n_ in groups])]), dtype=torch.int32,
                            device=dev)
@@ -643,4 +644,5 @@ def test_row_attention_matches_torch_and_grouped_is_bit_identical(append):
                                              ng.data_ptr(), len(groups) + 2, out2.data_ptr(), out2.stride(0), H, D,
                                              0.125, st), "attn_grouped")
         torch.cuda.synchronize()
-        assert torch.equal(out2, out)
+        for r in range(R):
+            assert torch.allclose(out2[r].float(), refs[r], atol=2e-2, rtol=2e-2), f"grouped row {r}"
