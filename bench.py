@@ -105,6 +105,38 @@ def cpu_reference(w, corpus, per_proc: int, procs: int | None = None):
     return total / busy, len(shards), txt, wall
 
 
+def cpu_search_only(w, beams: int = 8, seed: int = 0):
+    """search-only expand_beam throughput of the reference
+    algorithm (oracle port of bb/search.py:76-145) on replayed rows — k active
+    candidates per beam, fp64 log-softmax rows of |V| — in logits/s on one
+    core (the rows are made outside the timed region)."""
+    import numpy as np
+
+    from oracle import varstream_oracle as O
+
+    rng = np.random.default_rng(seed)
+    cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"],
+                    max_candidates=w["M"], max_len=w["max_len"])
+    V, k = w["V"], w["k"]
+    cases = []
+    for b in range(beams):
+        cands = tuple(O.Candidate(tokens=(w["sos"], 5 + i), score=-0.1 * i, finalized=False, input_id=b)
+                      for i in range(k))
+        beam = O.Beam(input_id=b, candidates=cands, l_t=2, emitted=0)
+        x = -w["scale"] * np.log2(rng.random((k, V)).clip(2.0 ** -24))
+        rows = x - (x.max(axis=1, keepdims=True) + np.log(np.exp(x - x.max(axis=1, keepdims=True))
+                                                          .sum(axis=1, keepdims=True)))
+        cases.append((beam, list(rows)))
+    t0 = time.perf_counter()
+    for beam, rows in cases:
+        O.expand_beam(beam, rows, cfg, V, w["eos"])
+    dt = time.perf_counter() - t0
+    return {"value": round(beams * k * V / dt, 1), "unit": "logits/s", "cores": 1, "kind": "port",
+            "sample": f"{beams} beams x {k} active rows x |V|={V} (fp64 log-softmax rows), expand_beam only; "
+                      "the port selects each row's top-M with numpy partition, far faster than the "
+                      "reference's per-row Python sort (SURVEY §8(a) a2: 1.2-2.4 M logits/s/core)"}
+
+
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
@@ -554,7 +586,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
-                                "sample": txt}
+                                "sample": txt, "search_only": cpu_search_only(w)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
