@@ -335,11 +335,12 @@ class GraphedTransformerScorer(TransformerScorer):
             qkv = x @ L["qkv"].T
             self._row_attn(qkv[:, :d], self.kv[li, 0], self.kv[li, 1], phys_kv, ln, qkv[:, d:2 * d],
                        qkv[:, 2 * d:], att)
-            x = F.layer_norm(x + att @ L["o"].T, (d,))
+            # residual adds in the GEMM epilogue (addmm: one rounding, no separate add kernel)
+            x = F.layer_norm(torch.addmm(x, att, L["o"].T), (d,))
             cq = x @ L["cq"].T
             self._row_attn_grouped(cq, self.enc_kv[li, 0], self.enc_kv[li, 1], slot, enc_len, att)
-            x = F.layer_norm(x + att @ L["co"].T, (d,))
-            x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (d,))
+            x = F.layer_norm(torch.addmm(x, att, L["co"].T), (d,))
+            x = F.layer_norm(torch.addmm(x, F.gelu(x @ L["f1"].T), L["f2"].T), (d,))
         lg = self.lg[:Rb, : self.vocab.size]
         eos = self.vocab.eos
         src_len = t["slot_src_len"][slot.long()].float()
