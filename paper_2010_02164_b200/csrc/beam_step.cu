@@ -189,23 +189,54 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   const double cutoff = s_cut;
   // ---- ranks of entries at/above the cutoff --------------------------------------
   const int kk = P < k ? P : k;
-  int mine = 0;
-  for (int e = tid; e < P; e += NT2) {
-    if (!(ps[e] >= cutoff)) continue;  // pruned by the absolute threshold (inclusive)
-    int rank = 0;
-    for (int Lh = 0; Lh < NL && rank < kk; ++Lh) {
-      const int b0 = Lh < nfz ? Lh : nfz + (Lh - nfz) * Meff;
-      const int len = Lh < nfz ? 1 : Meff;
-      for (int q = 0; q < len && pool.before(b0 + q, e); ++q) ++rank;  // list is sorted
+  int nkept;
+  if (P > 160 && P <= 512) {
+    // wide pools: a bitonic sort of the pool indices in proposal order (a
+    // strict total order, so the result is the same as ranking each entry);
+    // entries at/above the cutoff are a prefix of it (the order is score-first)
+    __shared__ short sidx[512];
+    int Pp = 256;
+    while (Pp < P) Pp <<= 1;
+    for (int i = tid; i < Pp; i += NT2) sidx[i] = i < P ? (short)i : (short)-1;
+    __syncthreads();
+    for (int kb = 2; kb <= Pp; kb <<= 1)
+      for (int j = kb >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < Pp; i += NT2) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int a = sidx[i], c = sidx[ixj];
+            const bool a_first = c < 0 || (a >= 0 && pool.before(a, c));
+            if (((i & kb) == 0) != a_first) {
+              sidx[i] = (short)c;
+              sidx[ixj] = (short)a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    const int e = tid < kk ? sidx[tid] : -1;  // kk <= k <= NT2: one rank per thread
+    const bool in = e >= 0 && ps[e] >= cutoff;
+    if (in) kept[tid] = e;
+    nkept = __syncthreads_count(in);
+  } else {
+    int mine = 0;
+    for (int e = tid; e < P; e += NT2) {
+      if (!(ps[e] >= cutoff)) continue;  // pruned by the absolute threshold (inclusive)
+      int rank = 0;
+      for (int Lh = 0; Lh < NL && rank < kk; ++Lh) {
+        const int b0 = Lh < nfz ? Lh : nfz + (Lh - nfz) * Meff;
+        const int len = Lh < nfz ? 1 : Meff;
+        for (int q = 0; q < len && pool.before(b0 + q, e); ++q) ++rank;  // list is sorted
+      }
+      if (rank < kk) {
+        kept[rank] = e;
+        ++mine;
+      }
     }
-    if (rank < kk) {
-      kept[rank] = e;
-      ++mine;
-    }
+    if (mine) atomicAdd(&s_kept, mine);
+    __syncthreads();
+    nkept = s_kept;  // ranks 0..nkept-1 are filled (contiguous prefix)
   }
-  if (mine) atomicAdd(&s_kept, mine);
-  __syncthreads();
-  const int nkept = s_kept;  // ranks 0..nkept-1 are filled (contiguous prefix)
 
   // ---- materialise children (thread j = child j) --------------------------------
   const int j = tid;
