@@ -15,6 +15,7 @@
 // also written into the cache (the self-attention append), so the cache
 // write and the attention are one launch.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace vs {
 namespace {
@@ -210,6 +211,162 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Tiled per-row attention (the self-attention with append): the CTA's K and V
+// slices (HPC heads x 32 positions) are staged into shared memory with
+// cp.async, double-buffered, so a whole tile (32 KB) is in flight per CTA
+// instead of one 128-byte line per lane; 16-byte chunks are XOR-swizzled by
+// position so lanes over positions read conflict-free.  Online softmax per
+// tile (lane = position), V accumulated from shared memory.
+constexpr int TP = 32;   // positions per tile
+constexpr int TBUF = 1;  // tile buffers per CTA (32 KB of smem: 6 CTAs per SM; other CTAs overlap the refill)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(HPC * 32, 6) row_attention_tiled_kernel(
+    const __nv_bfloat16* __restrict__ q, int64_t q_ld, __nv_bfloat16* __restrict__ kc,
+    __nv_bfloat16* __restrict__ vc, int64_t row_stride, int64_t pos_stride, const int* __restrict__ idx,
+    const int* __restrict__ lens, const __nv_bfloat16* __restrict__ knew, const __nv_bfloat16* __restrict__ vnew,
+    int64_t new_ld, __nv_bfloat16* __restrict__ out, int64_t out_ld, int H, float scale, int R_host,
+    const int* __restrict__ d_R) {
+  VS_PDL_ENTRY();
+  extern __shared__ __align__(128) uint4 tsm[];  // K [TBUF][TP][HPC][8], V [TBUF][TP][HPC][8]
+  __shared__ float sp[HPC][TP];
+  __shared__ uint4 qs[HPC][DH / 8];  // this row's q for the CTA's heads (broadcast reads)
+  uint4* Kt = tsm;
+  uint4* Vt = tsm + TBUF * TP * HPC * 8;
+  const int r = blockIdx.x;
+  const int R = d_R ? *d_R : R_host;
+  if (r >= R) return;
+  const int tid = threadIdx.x, hw = tid >> 5, lane = tid & 31;
+  const int hb = blockIdx.y * HPC;
+  const int h = hb + hw;
+  const int L = lens[r];
+  const int64_t row = idx[r];
+  const bool has_new = knew != nullptr;
+  if (has_new && lane < DH / 8 && h < H) {  // append: write the new K/V line into the cache
+    const int64_t dst = row * row_stride + (int64_t)(L - 1) * pos_stride + (int64_t)h * DH + lane * 8;
+    const int64_t src = (int64_t)r * new_ld + (int64_t)h * DH + lane * 8;
+    *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(knew + src);
+    *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(vnew + src);
+  }
+  const int ntile = (L + TP - 1) / TP;
+  // stage tile `t` into buffer `bf`: TP positions x HPC heads x 8 chunks, K and V
+  auto stage = [&](int t, int bf) {
+    for (int i = tid; i < TP * HPC * 8; i += HPC * 32) {
+      const int c = i & 7, hh = (i >> 3) % HPC, pl = i / (8 * HPC);
+      const int pos = t * TP + pl;
+      if (pos >= L || hb + hh >= H) continue;
+      const int64_t hoff = (int64_t)(hb + hh) * DH;
+      const __nv_bfloat16 *ks, *vs;
+      if (has_new && pos == L - 1) {  // the newest position from k_new/v_new (not via the cache write)
+        ks = knew + (int64_t)r * new_ld + hoff;
+        vs = vnew + (int64_t)r * new_ld + hoff;
+      } else {
+        ks = kc + row * row_stride + (int64_t)pos * pos_stride + hoff;
+        vs = vc + row * row_stride + (int64_t)pos * pos_stride + hoff;
+      }
+      const int d = ((bf * TP + pl) * HPC + hh) * 8 + (c ^ (pl & 7));
+      cp_async16(Kt + d, reinterpret_cast<const uint4*>(ks) + c);
+      cp_async16(Vt + d, reinterpret_cast<const uint4*>(vs) + c);
+    }
+  };
+  stage(0, 0);
+  cp_commit();
+  if (TBUF > 1 && ntile > 1) stage(1, 1);
+  cp_commit();
+  if (h < H && lane < DH / 8)
+    qs[hw][lane] = reinterpret_cast<const uint4*>(q + (int64_t)r * q_ld + (int64_t)h * DH)[lane];
+  const int g = lane >> 3, sub = lane & 7;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  float m = -INFINITY, l = 0.f;
+  for (int t = 0; t < ntile; ++t) {
+    const int bf = t % TBUF;
+    if (TBUF > 1) cp_wait<1>();
+    else cp_wait<0>();
+    __syncthreads();
+    if (h < H) {
+      const int pl = lane, pos = t * TP + pl;
+      float sc = -INFINITY;
+      if (pos < L) {
+        const uint4* kl = Kt + ((bf * TP + pl) * HPC + hw) * 8;
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) {
+          const uint4 kv = kl[c ^ (pl & 7)];
+          const uint4 qv = qs[hw][c];
+          const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+          const uint32_t qc[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 a = bf2(qc[u]), b = bf2(kw[u]);
+            acc0 = fmaf(a.x, b.x, acc0);
+            acc1 = fmaf(a.y, b.y, acc1);
+          }
+        }
+        sc = (acc0 + acc1) * scale;
+      }
+      float mx = sc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float mn = fmaxf(m, mx);
+      const float cr = m == -INFINITY ? 0.f : __expf(m - mn);
+      const float p = pos < L ? __expf(sc - mn) : 0.f;
+      float ps = p;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      l = l * cr + ps;
+      m = mn;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] *= cr;
+      sp[hw][pl] = p;
+      __syncwarp();
+      const int nt = min(TP, L - t * TP);
+      for (int t0 = 0; t0 < nt; t0 += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int pl2 = t0 + 4 * u + g;
+          if (pl2 < nt) {
+            const uint4 vv = Vt[((bf * TP + pl2) * HPC + hw) * 8 + (sub ^ (pl2 & 7))];
+            const float pp = sp[hw][pl2];
+            const uint32_t w4[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              const float2 v = bf2(w4[q2]);
+              acc[2 * q2] = fmaf(pp, v.x, acc[2 * q2]);
+              acc[2 * q2 + 1] = fmaf(pp, v.y, acc[2 * q2 + 1]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // buffer bf is free again
+    if (t + TBUF < ntile) stage(t + TBUF, bf);
+    cp_commit();
+  }
+  if (h >= H) return;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 8);
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+  }
+  if (g == 0) {
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint4 o;
+    o.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    o.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    o.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+    o.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(out + (int64_t)r * out_ld + (int64_t)h * DH + sub * 8) = o;
+  }
+}
+
 constexpr int GROWS = 64;  // query rows per CTA pass (4 warps x 16)
 __global__ void __launch_bounds__(128) row_attention_grouped_kernel(
     const __nv_bfloat16* __restrict__ q, int64_t q_ld, const __nv_bfloat16* __restrict__ kc,
@@ -365,11 +522,31 @@ extern "C" int vs_row_attention(const void* q, int64_t q_ld, void* k_cache, void
       R_grid < 0 || ((k_new == nullptr) != (v_new == nullptr)))
     return VS_ERR_CONFIG;
   if (R_grid == 0) return VS_OK;
-  vs::vs_launch(vs::row_attention_kernel, dim3(R_grid, heads / vs::HPC), dim3(32 * vs::HPC), 0, static_cast<cudaStream_t>(stream), 
-      static_cast<const __nv_bfloat16*>(q), q_ld, static_cast<__nv_bfloat16*>(k_cache),
-      static_cast<__nv_bfloat16*>(v_cache), row_stride, pos_stride, idx, lens,
-      static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new), new_ld,
-      static_cast<__nv_bfloat16*>(out), out_ld, heads, scale, R_host, d_R);
+  static int tiled = -1;  // VS_ATTN_TILED=0: the register kernel (one K line per lane in flight)
+  if (tiled < 0) {
+    const char* e = getenv("VS_ATTN_TILED");
+    tiled = e ? atoi(e) : 1;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (tiled) {
+    const size_t dsm = 2 * vs::TBUF * vs::TP * vs::HPC * 8 * sizeof(uint4);  // K and V tiles
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(vs::row_attention_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+      attr = true;
+    }
+    vs::vs_launch(vs::row_attention_tiled_kernel, dim3(R_grid, heads / vs::HPC), dim3(32 * vs::HPC), dsm, st,
+                  static_cast<const __nv_bfloat16*>(q), q_ld, static_cast<__nv_bfloat16*>(k_cache),
+                  static_cast<__nv_bfloat16*>(v_cache), row_stride, pos_stride, idx, lens,
+                  static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new), new_ld,
+                  static_cast<__nv_bfloat16*>(out), out_ld, heads, scale, R_host, d_R);
+  } else {
+    vs::vs_launch(vs::row_attention_kernel, dim3(R_grid, heads / vs::HPC), dim3(32 * vs::HPC), 0, st,
+                  static_cast<const __nv_bfloat16*>(q), q_ld, static_cast<__nv_bfloat16*>(k_cache),
+                  static_cast<__nv_bfloat16*>(v_cache), row_stride, pos_stride, idx, lens,
+                  static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new), new_ld,
+                  static_cast<__nv_bfloat16*>(out), out_ld, heads, scale, R_host, d_R);
+  }
   VS_CUDA_RET();
 }
 
