@@ -630,7 +630,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="wmt19_k50")
     ap.add_argument("--n-inputs", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-per-proc", type=int, default=6)
+    ap.add_argument("--cpu-per-proc", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent refilling batches (n slots each) per GPU, on separate CUDA streams")

@@ -46,7 +46,8 @@ def _check_rows(x32: np.ndarray, M: int, tok, lp, lse, normalized=False):
 
 
 CASES = [(1000, 3), (1000, 5), (2048, 10), (42024, 5), (42024, 50), (17, 3), (3, 5), (4096, 1),
-         (33, 16), (1001, 64), (65535, 5), (65536, 7)]  # 32-bit / 64-bit top-list keys
+         (33, 16), (1001, 64), (65535, 5), (65536, 7),  # 32-bit / 64-bit top-list keys
+         (4096, 32), (4096, 33)]  # largest register top-list / smallest buffered-candidate M
 
 
 @pytest.mark.parametrize("kernel", ["split", "warp"])
