@@ -581,7 +581,7 @@ extern "C" int vs_proj_lse_topm(const void* H, int64_t ldh, const void* W, int64
   CUtensorMap mh, mw;
   static int CLn = -1;
   if (CLn < 0) {
-    // 1: single CTAs; 2: CTA pairs multicasting W; 3: CTA pairs with cta_group::2 MMA (default)
+    // 1: single CTAs; 2 (default): CTA pairs multicasting W; 3: CTA pairs with cta_group::2 MMA
     const char* c = getenv("VS_K5_CL");
     CLn = c ? atoi(c) : 2;
     if (CLn < 1 || CLn > 3) CLn = 2;
