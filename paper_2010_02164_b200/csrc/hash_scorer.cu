@@ -53,6 +53,10 @@ __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __
 // Persistent grid-stride over (row, 2048-column chunk) work items with the
 // live row count read from device memory: no empty CTAs are launched for
 // rows beyond R_t.  8 consecutive tokens per thread, one 16-byte store (bf16).
+// Each thread writes HVPT 16-byte groups of 8 logits per (row, chunk) work item,
+// so the per-item row lookups are amortised; the EOS value (a division) is only
+// computed in the one group that holds EOS.
+constexpr int HVPT = 2;
 template <typename T>
 __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_state st, vs_hash_params hp,
                                                           T* __restrict__ logits, int64_t ld, int cols) {
@@ -61,35 +65,38 @@ __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_stat
   const int V = cfg.vocab_size;
   for (int w = blockIdx.x; w < R * cols; w += gridDim.x) {
     const int r = w / cols, cchunk = w - r * cols;
-    const int v0 = (cchunk * blockDim.x + threadIdx.x) * 8;
-    if (v0 >= V) continue;
     const int s = st.row_slot[r];
     const uint64_t h = st.c_hash[s * cfg.k + st.row_cand[r]];
     const uint32_t key = (uint32_t)(h ^ (h >> 32));
-    const float eos_val =
-        __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
     T* out = logits + (int64_t)r * ld;
-    T vals[8];
-    if ((unsigned)(cfg.eos - v0) < 8u) {  // the one chunk holding EOS
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int v = v0 + j;
-        vals[j] = cvt<T>((v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power));
-      }
-    } else {
+    for (int g = 0; g < HVPT; ++g) {
+      const int v0 = ((cchunk * HVPT + g) * blockDim.x + threadIdx.x) * 8;
+      if (v0 >= V) continue;
+      T vals[8];
+      if ((unsigned)(cfg.eos - v0) < 8u) {  // the one group holding EOS
+        const float eos_val =
+            __fdiv_rn(__fmul_rn(hp.eos_bias, (float)st.row_len[r]), (float)st.slot_src_len[s]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) vals[j] = cvt<T>(hash_logit(key, v0 + j, hp.scale, hp.power));
-    }
-    const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
-    if (vec_ok) {
-      if (sizeof(T) == 2) {
-        *reinterpret_cast<uint4*>(out + v0) = *reinterpret_cast<const uint4*>(vals);
+        for (int j = 0; j < 8; ++j) {
+          const int v = v0 + j;
+          vals[j] = cvt<T>((v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power));
+        }
       } else {
-        reinterpret_cast<uint4*>(out + v0)[0] = reinterpret_cast<const uint4*>(vals)[0];
-        reinterpret_cast<uint4*>(out + v0)[1] = reinterpret_cast<const uint4*>(vals)[1];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vals[j] = cvt<T>(hash_logit(key, v0 + j, hp.scale, hp.power));
       }
-    } else {
-      for (int j = 0; j < 8 && v0 + j < V; ++j) out[v0 + j] = vals[j];
+      const bool vec_ok = (v0 + 8 <= V) && ((reinterpret_cast<uintptr_t>(out + v0) & 15) == 0);
+      if (vec_ok) {
+        if (sizeof(T) == 2) {
+          *reinterpret_cast<uint4*>(out + v0) = *reinterpret_cast<const uint4*>(vals);
+        } else {
+          reinterpret_cast<uint4*>(out + v0)[0] = reinterpret_cast<const uint4*>(vals)[0];
+          reinterpret_cast<uint4*>(out + v0)[1] = reinterpret_cast<const uint4*>(vals)[1];
+        }
+      } else {
+        for (int j = 0; j < 8 && v0 + j < V; ++j) out[v0 + j] = vals[j];
+      }
     }
   }
 }
@@ -109,7 +116,7 @@ extern "C" int vs_hash_logits(const vs_config* cfg, const vs_state* st, const vs
   if (!cfg || !st || !hp || !logits || ld < cfg->vocab_size) return VS_ERR_CONFIG;
   if (hp->power != 0 && hp->power != 1 && hp->power != 2 && hp->power != 4) return VS_ERR_CONFIG;
   if (R_grid <= 0) return VS_OK;
-  const int cols = (cfg->vocab_size + 8 * 256 - 1) / (8 * 256);
+  const int cols = (cfg->vocab_size + 8 * 256 * vs::HVPT - 1) / (8 * 256 * vs::HVPT);
   static int sms = 0;
   if (!sms) {
     int dev = 0;
