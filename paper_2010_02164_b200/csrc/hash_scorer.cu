@@ -43,6 +43,12 @@ __device__ __forceinline__ float hash_logit(uint32_t key, int v, float scale, in
   return __fmul_rn(u, scale);
 }
 
+__device__ __forceinline__ unsigned long long pk2f(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 template <typename T>
 __device__ __forceinline__ T cvt(float x);
 template <>
@@ -81,6 +87,24 @@ __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_stat
         for (int j = 0; j < 8; ++j) {
           const int v = v0 + j;
           vals[j] = cvt<T>((v == cfg.eos) ? eos_val : hash_logit(key, v, hp.scale, hp.power));
+        }
+      } else if (hp.power == 0) {  // log-like, two elements per packed multiply (same roundings)
+        float lg[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t bits = fmix32(((uint32_t)(v0 + j) * 0x9E3779B9u) ^ key);
+          lg[j] = (float)(int)(__float_as_uint((float)((bits >> 8) + 1u)) - 0x4B800000u);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          unsigned long long t;
+          asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2f(lg[j], lg[j + 1])),
+              "l"(pk2f(1.1920928955078125e-07f, 1.1920928955078125e-07f)));
+          asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(t) : "l"(pk2f(-hp.scale, -hp.scale)));
+          float a, b;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(t));
+          vals[j] = cvt<T>(a);
+          vals[j + 1] = cvt<T>(b);
         }
       } else {
 #pragma unroll
