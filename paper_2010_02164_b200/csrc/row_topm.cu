@@ -4,19 +4,20 @@
 // bb/search.py:63-73 (_candidate_pool: first M of sorted(range(V),
 // key=(-row[t], t))), for every scored row of a timestep at once.
 //
-// One WARP per row (4 independent warps per CTA, no block barriers).  The row
-// is read from HBM exactly once: 16-byte non-allocating vector loads, U
-// vectors per lane per batch, double-buffered so the next batch is in flight
-// while the current one is reduced.  Per element the hot loop does only the
-// online log-sum-exp (max, ex2, add) and one compare against a WARP-UNIFORM
-// candidate threshold θ (a 64-bit (logit, token) key):
-//   * θ is bootstrapped from a shuffle bitonic sort of the first batch's 32
-//     lane maxima (θ = M-th largest), so after the first batch only ~M·ln(V)
-//     elements ever pass the filter;
-//   * passing elements are appended to a per-warp shared-memory buffer with
-//     ballot/popc compaction; when it fills, M argmax rounds keep the top-M
-//     and raise θ (partial-sort merge).
-// Epilogue: warp-reduce lse, re-key the buffer by the contract value
+// W warps per row (W from the device-side row count, 8 warps per CTA).  The row
+// is read from HBM exactly once: 16-byte non-allocating vector loads, U vectors
+// per lane per batch, double-buffered in registers (or a per-warp shared-memory
+// ring filled by cp.async.bulk).  Per element the hot loop does only the online
+// log-sum-exp (FFMA2, ex2, FADD2) against a warp-uniform, lazily raised max, and
+// per vector one compare of its max against a warp-uniform candidate threshold
+// θ (one warp vote guards both rare paths):
+//   * M <= 32: candidates live in a register top-list (lane j holds the j-th
+//     key; 32-bit keys for bf16 rows with |V| < 65536), seeded from the lane
+//     maxima of the first two batches, so θ is always the exact M-th key;
+//   * M > 32: passing elements are appended to a per-warp shared-memory buffer
+//     (ballot compaction); when it fills, M argmax rounds keep the top-M and
+//     raise θ.
+// Epilogue: warp-reduce lse, re-key the candidates by the contract value
 // logp = fp32(x - lse) with token-ascending ties, M warp-argmax rounds, and an
 // exact verification that no element filtered out by θ can reach the M-th
 // (logp, token) key — tie-aware, using the next-smaller representable input
