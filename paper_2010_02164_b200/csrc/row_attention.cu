@@ -7,10 +7,15 @@
 // read in place — no gather of K/V into a dense batch — so a step reads each
 // live candidate's prefix exactly once: R * len * 2 * H * Dh * 2 bytes.
 //
-// CTA per row, one warp per head (Dh = 64).  Scores: lane t owns positions
-// t, t+32, ... (one 128-byte K line per position, q in registers), softmax by
-// warp reductions in fp32, then the output with lanes over head dims (two
-// per lane, 128-byte coalesced V lines, probabilities broadcast by shuffle).
+// Three kernels, one warp per (row, head) unit of work (Dh = 64):
+//   * row_attention_tiled_kernel (default for vs_row_attention): CTA per (row,
+//     4 heads); the row's K/V slices are staged per 32-position tile into
+//     shared memory with cp.async (XOR-swizzled chunks), scores with lane =
+//     position, online softmax in fp32, V accumulated from shared memory;
+//   * row_attention_kernel (VS_ATTN_TILED=0): the same per row, straight from
+//     global memory (one 128-byte K line per lane in flight);
+//   * row_attention_grouped_kernel (vs_row_attention_grouped, cross-attention):
+//     rows of one beam share the slot's encoder states; mma.m16n8k16 tiles.
 // With `knew`/`vnew` the row's newest position (len-1) is taken from them and
 // also written into the cache (the self-attention append), so the cache
 // write and the attention are one launch.
