@@ -21,6 +21,7 @@ a ring of status snapshots; used for throughput).
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import math
 from dataclasses import dataclass
 from typing import Callable, Sequence
@@ -162,8 +163,8 @@ class SearchEngine:
             lens = np.fromiter((len(x) for x in corpus), dtype=np.int64, count=len(corpus))
             src_off = np.zeros(len(corpus) + 1, dtype=np.int32)
             np.cumsum(lens, out=src_off[1:])
-            src_tok = np.fromiter((t for x in corpus for t in x), dtype=np.int32,
-                                  count=int(src_off[-1]))
+            src_tok = np.fromiter(itertools.chain.from_iterable(corpus), dtype=np.int32,
+                                  count=int(src_off[-1]))  # C-level flattening
         if isinstance(src_off, np.ndarray):
             src_off, src_tok = torch.from_numpy(src_off), torch.from_numpy(src_tok)
         n_in = int(src_off.shape[0]) - 1
