@@ -96,3 +96,24 @@ def test_metrics_rounding_goldens():
     for row in load("metrics.json"):
         r = MetricsReport(timesteps=row["steps"], candidate_expansions=row["expansions"])
         assert r.summarize() == row["summary"]
+
+
+def test_every_entry_rejects_bad_arguments_before_touching_the_device(lib):
+    """Each C-ABI entry validates its host-side arguments first and returns
+    VS_ERR_CONFIG (-> ConfigError) without a CUDA call (this runs without a GPU)."""
+    from paper_2010_02164_b200 import _native as N
+
+    E = N.VS_ERR_CONFIG
+    assert lib.vs_row_lse_topm_ws(None, 0, 10, 10, 3, 1, None, 1, None, None, None, None, None, 0, None) == E
+    assert lib.vs_row_attention(None, 64, None, None, 0, 0, None, None, None, None, 0, None, 0, 16, 64,
+                                0.125, 1, None, 1, None) == E
+    assert lib.vs_row_attention_grouped(None, 64, None, None, 0, 0, None, None, None, None, 1, None, 0, 16,
+                                        64, 0.125, None) == E
+    assert lib.vs_proj_lse_topm(None, 1024, None, 1024, 1, None, 1, 1024, 100, 5, 2, None, None, 128, None,
+                                None, None, None, None, 0, None) == E
+    assert lib.vs_rows_copy(None, 0, 1, 0, 16, None, None, 1, None) == E
+    assert lib.vs_scatter_rows(None, 0, None, 0, 16, None, None, 1, None) == E
+    # head_dim other than 64 is a configuration error even with (dummy) pointers
+    buf = C.create_string_buffer(64)
+    p = C.addressof(buf)
+    assert lib.vs_row_attention_grouped(p, 64, p, p, 0, 0, p, p, p, p, 1, p, 0, 16, 32, 0.125, None) == E
