@@ -78,8 +78,9 @@ def _cpu_worker(args):
     cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"],
                     max_candidates=w["M"], max_len=w["max_len"])
     t0 = time.perf_counter()
-    _, rep = O.run_varstream(inputs, sc, cfg)
-    return time.perf_counter() - t0, rep.candidate_expansions
+    outs, rep = O.run_varstream(inputs, sc, cfg)
+    dt = time.perf_counter() - t0
+    return dt, rep.candidate_expansions, [[(c.tokens, c.score) for c in per] for per in outs]
 
 
 def cpu_reference(w, corpus, per_proc: int, procs: int | None = None):
@@ -90,19 +91,42 @@ def cpu_reference(w, corpus, per_proc: int, procs: int | None = None):
     procs = procs or min(os.cpu_count() or 1, 64)
     total = min(len(corpus), per_proc * procs)
     stride = max(1, len(corpus) // total)
-    sample = corpus[::stride][:total]
-    shards = [sample[q::procs] for q in range(procs)]
-    shards = [s for s in shards if s]
+    ids = list(range(0, len(corpus), stride))[:total]
+    sample = [corpus[i] for i in ids]
+    keep = [q for q in range(procs) if sample[q::procs]]
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
-    with ctx.Pool(len(shards)) as pool:
-        res = pool.map(_cpu_worker, [(w, s) for s in shards])
+    with ctx.Pool(len(keep)) as pool:
+        res = pool.map(_cpu_worker, [(w, sample[q::procs]) for q in keep])
     wall = time.perf_counter() - t0
     busy = max(r[0] for r in res)
     exp = sum(r[1] for r in res)
     txt = (f"{total} of {len(corpus)} inputs (every {stride}th of the length-sorted corpus), "
-           f"{len(shards)} processes x 1 thread, {exp} expansions, slowest shard {busy:.1f}s")
-    return total / busy, len(shards), txt, wall
+           f"{len(keep)} processes x 1 thread, {exp} expansions, slowest shard {busy:.1f}s")
+    cpu_outs = {}
+    for q, r in zip(keep, res):
+        cpu_outs.update(zip(ids[q::procs], r[2]))
+    return total / busy, len(keep), txt, wall, cpu_outs
+
+
+def agreement(cpu_outs, gpu_outs):
+    """north_star: end-to-end outputs vs the reference algorithm computing its
+    own fp64 log-softmax rows (no lse replay) on the same logits.  An input
+    agrees when its candidate token sequences are identical and every score is
+    within 1e-5 relative; returns the fraction and the worst score difference."""
+    same, worst = 0, 0.0
+    for i, want in cpu_outs.items():
+        got = [(c.tokens, c.score) for c in gpu_outs[i]]
+        ok = len(got) == len(want) and all(tuple(a[0]) == tuple(b[0]) for a, b in zip(got, want))
+        if ok:
+            rel = max((abs(a[1] - b[1]) / max(1e-12, abs(b[1])) for a, b in zip(got, want)), default=0.0)
+            worst = max(worst, rel)
+            ok = rel <= 1e-5
+        same += ok
+    n = max(1, len(cpu_outs))
+    return {"inputs": len(cpu_outs), "identical_fraction": round(same / n, 5),
+            "max_rel_score_diff": float(f"{worst:.3g}"),
+            "reference": "oracle port with fp64 log-softmax rows of the same bf16 logits (no lse replay)"}
 
 
 def cpu_search_only(w, beams: int = 8, seed: int = 0):
@@ -595,9 +619,10 @@ def run_ours(args):
         if args.decoder_cpu_baseline:  # ~3.5 min of host time: opt-in
             line["decoder_wmt19"]["cpu_baseline"] = decoder_cpu_baseline(w)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
+        v, cores, txt, _, cpu_outs = cpu_reference(w, local_corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
                                 "sample": txt, "search_only": cpu_search_only(w)}
+        line["reference_agreement"] = agreement(cpu_outs, outs)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -614,7 +639,7 @@ def run_reference(args):
     corpus = _corpus(w)
     vals = []
     for i in range(args.warmup + args.steps):
-        v, cores, txt, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
+        v, cores, txt, _, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
