@@ -591,7 +591,7 @@ def run_ours(args):
                    "expansions_per_step": round(rep.expansions_per_step, 1)},
         "roofline": {"kernel": "vs_row_lse_topm (K1)", "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4),
+                     "frac": round(achieved / peak, 4), "frac_of_nominal_8tbs": round(achieved / 8000.0, 4),
                      "traffic": (round(traffic_ratio * k1_bytes / max(1, len(k1)))
                                  if traffic_ratio else None),
                      "traffic_source": "ncu --set full of the full-width launch (L2 flushed): "
@@ -602,7 +602,8 @@ def run_ours(args):
         "roofline_full_width": {"kernel": "vs_row_lse_topm (K1)", "R": w["n"] * w["k"],
                                 "bytes": fw_bytes, "ms": round(fw_t * 1e3, 4),
                                 "achieved": round(fw_gbs, 1), "peak": peak, "unit": "GB/s",
-                                "frac": round(fw_gbs / peak, 4), "l2": "flushed (256 MB write)",
+                                "frac": round(fw_gbs / peak, 4), "frac_of_nominal_8tbs": round(fw_gbs / 8000.0, 4),
+                                "l2": "flushed (256 MB write)",
                                 "traffic": traffic_fw,
                                 "exact_fallback_rows": fw_fb},
         "e2e": {"value": round(e2e_value, 2), "unit": "seq/s", "h2d_bytes_per_step": h2d,
