@@ -624,6 +624,9 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
                                 "sample": txt, "search_only": cpu_search_only(w)}
         line["reference_agreement"] = agreement(cpu_outs, outs)
+        v1, _, txt1, _, _ = cpu_reference(w, local_corpus, per_proc=8, procs=1)  # 1 process too
+        line["cpu_baseline"]["single_process"] = {"value": round(v1, 3), "unit": "seq/s", "cores": 1,
+                                                  "sample": txt1}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
