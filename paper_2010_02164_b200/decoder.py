@@ -230,6 +230,8 @@ class GraphedTransformerScorer(TransformerScorer):
                  fused_head: bool = False):
         if d % heads or d // heads != 64:
             raise ValueError("GraphedTransformerScorer needs head_dim 64")
+        if max_src > 256:  # vs_row_attention_grouped stages <= 256 encoder positions per slot
+            raise ValueError("GraphedTransformerScorer needs max_src <= 256")
         super().__init__(vocab, d=d, heads=heads, layers=layers, enc_layers=enc_layers, ffn=ffn,
                          max_src=max_src, seed=seed, tau=tau, eos_bias=eos_bias, dtype=torch.bfloat16,
                          device=device)
