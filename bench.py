@@ -495,7 +495,7 @@ def run_ours(args):
         e0.record()
         for _ in range(args.steps):  # no per-kernel events inside: they would break the PDL chain
             reps.append(decode())
-            launches += sum(5 * e.launched_steps + 1 for e in (engs if S > 1 else [eng]))
+            launches += sum(3 * e.launched_steps + 1 for e in (engs if S > 1 else [eng]))
         e1.record()
         barrier()
     t_local = e0.elapsed_time(e1) / 1e3

@@ -125,7 +125,8 @@ typedef struct vs_state {
   int32_t* hist;         /* token history                               */
   /* scheduler */
   int32_t* live;         /* [n] slot ids in arrival order               */
-  int32_t* counters;     /* [8]: n_live, cursor, N                      */
+  int32_t* counters;     /* [8]: n_live, cursor, N, error, copy counter,
+                            CTA arrival counter (zero-initialised)      */
   int32_t* sel;          /* [n] selected slot ids, in advance order     */
   int32_t* sel_off;      /* [n+1] row offsets of selected beams         */
   int32_t* row_slot;     /* [capacity] slot of each scored row          */
@@ -145,10 +146,14 @@ typedef struct vs_state {
   float* top_logp;
   float* row_lse;        /* [capacity]                                  */
   /* KV / row-state copies planned by beam_step: (src_phys, dst_phys, len) */
-  int32_t* copy_list;    /* [capacity*3]                                */
-  int32_t* n_copy;       /* [1]                                         */
+  int32_t* copy_list;    /* [n*k*3]: <= k surviving children per beam   */
+  int32_t* n_copy;       /* [1] copies planned by the last beam step    */
   /* host-visible status (VS_STATUS_INTS(n)) */
   int32_t* status;
+  /* per candidate [n*k]: the beam's ACTIVE candidates in beam order, packed
+   * (cand | phys_row << 8), written by the beam step and by admission; the
+   * scheduler builds the next row list from it */
+  int32_t* c_act;
 } vs_state;
 
 /* Library identification / sanity. */
@@ -193,6 +198,15 @@ size_t vs_row_lse_topm_ws_bytes(int32_t R_grid, int32_t V, int32_t dtype);
  * asc) in top_tok/top_logp with M = min(2k, V). */
 int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_rows, void* stream);
 
+/* K2+K3 fused — the same beam step, whose LAST CTA to finish then runs the
+ * scheduler for the next step (vs_schedule with do_remove=1, first_call=0 and
+ * the given modes): one launch per search step after the row kernel.  The
+ * status header is also written to status_mirror (16 int32 in pinned host
+ * memory, or NULL), so a host-side ring needs no copy launch.  Replaces
+ * bb/scheduler.py:180-192 + the next iteration's :266-270. */
+int vs_beam_step_schedule(const vs_config* cfg, const vs_state* st, int32_t M_rows, int32_t N,
+                          int32_t admit_mode, int32_t select_mode, int32_t* status_mirror, void* stream);
+
 /* K3  compact_refill_select — replaces bb/scheduler.py:190-192 (stable
  * removal of finished beams), :94-116 + :237-240 + :266-268 (ε-refill),
  * :119-165 (min-l_t / FIFO / all selection with capacity packing) and builds
@@ -201,6 +215,11 @@ int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_rows, void*
  * previous step's finished flags first. */
 int vs_schedule(const vs_config* cfg, const vs_state* st, int32_t N, int32_t first_call,
                 int32_t do_remove, int32_t admit_mode, int32_t select_mode, void* stream);
+/* vs_schedule that also writes the status header to status_mirror (pinned
+ * host memory, 16 int32). */
+int vs_schedule_mirror(const vs_config* cfg, const vs_state* st, int32_t N, int32_t first_call,
+                       int32_t do_remove, int32_t admit_mode, int32_t select_mode, int32_t* status_mirror,
+                       void* stream);
 
 /* K4  row-state reorder — no reference equivalent (the reference scorer is
  * stateless; bb/core.py:170 copies token tuples).  Applies copy_list: for

@@ -48,7 +48,7 @@ STATE_FIELDS = [
     "slot_flags", "slot_seed", "c_score", "c_len", "c_row", "c_fin", "c_hash", "hist", "live",
     "counters", "sel", "sel_off", "row_slot", "row_cand", "row_phys", "row_len", "src_off",
     "src_tok", "out_count", "out_len", "out_score", "out_tok", "top_tok", "top_logp", "row_lse",
-    "copy_list", "n_copy", "status",
+    "copy_list", "n_copy", "status", "c_act",
 ]
 
 
@@ -62,7 +62,8 @@ class VsHashParams(C.Structure):
 
 
 # Every symbol include/varstream.h declares (checked by tests/test_native_exports.py).
-EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step", "vs_schedule", "vs_rows_copy",
+EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step",
+           "vs_beam_step_schedule", "vs_schedule", "vs_schedule_mirror", "vs_rows_copy",
            "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention", "vs_row_attention_grouped",
            "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes")
 
@@ -87,6 +88,8 @@ def load_library(path: Path | None = None) -> C.CDLL:
         "vs_row_lse_topm_ws_bytes": ([i32, i32, i32], C.c_size_t),
         "vs_beam_step": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, vp], i32),
         "vs_schedule": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp], i32),
+        "vs_schedule_mirror": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp, vp], i32),
+        "vs_beam_step_schedule": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, vp, vp], i32),
         "vs_rows_copy": ([vp, i64, i32, i64, i64, vp, vp, i32, vp], i32),
         "vs_scatter_rows": ([vp, i64, vp, i64, i64, vp, vp, i32, vp], i32),
         "vs_hash_encode": ([C.POINTER(VsConfig), C.POINTER(VsState), u64, vp], i32),

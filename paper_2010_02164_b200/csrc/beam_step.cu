@@ -28,7 +28,9 @@
 // get a (src,dst,len) copy entry.  Sources are always rows claimed by
 // inheritors, destinations always free rows, so in-place copies are
 // hazard-free.
-#include "common.cuh"
+#include <algorithm>
+
+#include "schedule.cuh"
 
 namespace vs {
 namespace {
@@ -66,11 +68,9 @@ __device__ __forceinline__ int block_prefix(bool pred, int* wsm, int* total) {
   return off + __popc(b & ((1u << lane) - 1u));
 }
 
-__global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows) {
-  VS_PDL_ENTRY();
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_state& st, int M_rows,
+                                              unsigned char* smem) {
   const int b = blockIdx.x;
-  if (b >= st.status[VS_ST_NSEL]) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int k = cfg.k;
   const int s = st.sel[b];
@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   int* nrow = emo + k;                                // [k] child row
   int* csrc = nrow + k;                               // [k] child copy source row (-1)
   int* nlen = csrc + k;                               // [k] child length
+  int* ctok = nlen + k;                               // [k] child's new token (-1: no-op)
+  int* prow = ctok + k;                               // [k] row holding the child's prefix
   __shared__ int wsm[NT2 / 32];
-  __shared__ int s_kept;
+  __shared__ int s_kept, s_nextra;
   __shared__ double s_cut;
 
   // ---- candidates -> smem; stable finalized / active split ---------------------
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   __syncthreads();
   const int P = nfz + nact * Meff;
 
+  VS_PROF(blockIdx.x == 0, 1);
   // ---- pool (bb/search.py:64-72): no-ops, then per-parent top-M ----------------
   for (int e = tid; e < P; e += NT2) {
     if (e < nfz) {
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   __syncthreads();
   const Pool pool{ps, pp, pt};
   const int NL = nfz + nact;  // == w lists
+  VS_PROF(blockIdx.x == 0, 2);
   // ---- rank-0 entry = best list head (warp 0) -> δ cutoff ------------------------
   if (wid == 0) {
     int best = -1;
@@ -238,6 +242,7 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
     nkept = s_kept;  // ranks 0..nkept-1 are filled (contiguous prefix)
   }
 
+  VS_PROF(blockIdx.x == 0, 3);
   // ---- materialise children (thread j = child j) --------------------------------
   const int j = tid;
   const bool child = j < nkept;
@@ -280,13 +285,20 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
     const int fpos = block_prefix(fr, wsm, &nfree);
     if (fr) freel[fpos] = tid;
     const int xpos = block_prefix(extra, wsm, &nextra);  // barrier inside orders freel
-    if (extra) crow = freel[xpos];
+    if (extra) {
+      crow = freel[xpos];
+      act[xpos] = j;  // the pool is built: act[] now lists the extra children
+    }
+    if (tid == 0) s_nextra = nextra;
   }
   if (child) {
     nrow[j] = crow;
     csrc[j] = src;
     nlen[j] = clen;
+    ctok[j] = tk;
+    prow[j] = cr[pi];  // a no-op's own row, else the parent's (prefix [0, L))
   }
+  VS_PROF(blockIdx.x == 0, 4);
   // ---- deferred emission + length-cap drain ------------------------------------
   const int emitted0 = st.slot_emitted[s];
   int first, ne, width;
@@ -316,33 +328,52 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
     }
   }
   __syncthreads();
-  // ---- token histories: copy parent prefixes into new rows (warp per child) ----
+  VS_PROF(blockIdx.x == 0, 5);
+  // ---- token histories + emission, one flattened phase ---------------------------
+  // Every read is of a claimed row's prefix [0, L) (a parent's, or a no-op's own
+  // row), every write goes to a free row or to position L, so the prefix copies
+  // of extra children, the appends and the emissions (read from the prefix row
+  // + the new token) are independent: no barrier between them, loads batched.
   const int ML = cfg.max_len;
-  for (int c = wid; c < nkept; c += NT2 / 32) {
-    const int sr = csrc[c];
-    if (sr < 0) continue;
-    const int32_t* srcp = st.hist + (int64_t)(base + sr) * ML;
-    int32_t* dstp = st.hist + (int64_t)(base + nrow[c]) * ML;
-    for (int p = lane; p < L; p += 32) dstp[p] = srcp[p];
-  }
-  __syncthreads();
-  if (child && tk >= 0) st.hist[(int64_t)(base + crow) * ML + L] = tk;
-  __syncthreads();
-
-  // ---- emission into the per-input output buffers (warp per emission) ---------
   const int input = st.slot_input[s];
-  for (int q = wid; q < ne; q += NT2 / 32) {
-    const int c = emo[q];
-    const int64_t o = (int64_t)input * k + emitted0 + q;
-    const int32_t* srcp = st.hist + (int64_t)(base + nrow[c]) * ML;
-    const int len = nlen[c];
-    for (int p = lane; p < len; p += 32) st.out_tok[o * ML + p] = srcp[p];
-    if (lane == 0) {
-      st.out_len[o] = len;
-      st.out_score[o] = ps[kept[c]];
+  const int nextra = s_nextra;
+  if (child && tk >= 0) st.hist[(int64_t)(base + crow) * ML + L] = tk;
+  if (j < ne) {
+    const int c = emo[j];
+    const int64_t o = (int64_t)input * k + emitted0 + j;
+    st.out_len[o] = nlen[c];
+    st.out_score[o] = ps[kept[c]];
+  }
+  {
+    const int T1 = nextra * L, T = T1 + ne * (L + 1);
+    constexpr int U = 4;
+    for (int i0 = tid; i0 < T; i0 += NT2 * U) {
+      int val[U];
+      int32_t* dst[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NT2;
+        dst[u] = nullptr;
+        if (i < T1) {  // prefix copy of extra child act[x]
+          const int x = i / L, p = i - x * L, c = act[x];
+          val[u] = st.hist[(int64_t)(base + csrc[c]) * ML + p];
+          dst[u] = st.hist + (int64_t)(base + nrow[c]) * ML + p;
+        } else if (i < T) {  // token p of emission q
+          const int q = (i - T1) / (L + 1), p = (i - T1) - q * (L + 1), c = emo[q];
+          if (p < nlen[c]) {
+            const bool last = ctok[c] >= 0 && p == nlen[c] - 1;
+            val[u] = last ? ctok[c] : st.hist[(int64_t)(base + prow[c]) * ML + p];
+            dst[u] = st.out_tok + ((int64_t)input * k + emitted0 + q) * ML + p;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u]) *dst[u] = val[u];
     }
   }
 
+  VS_PROF(blockIdx.x == 0, 6);
   // ---- next beam SoA, KV copy plan, slot state ---------------------------------
   const bool stays = child && j >= first && j < first + width;
   if (stays) {
@@ -353,13 +384,15 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
     st.c_row[base + d] = crow;
     st.c_fin[base + d] = (uint8_t)cfin;
     if (src >= 0 && !cfin) {  // only active children are scored again
-      const int slot = atomicAdd(st.n_copy, 1);
+      const int slot = atomicAdd(&st.counters[4], 1);  // published as *n_copy by the last CTA
       st.copy_list[3 * slot + 0] = base + src;
       st.copy_list[3 * slot + 1] = base + crow;
       st.copy_list[3 * slot + 2] = L;
     }
   }
-  const int nact2 = __syncthreads_count(stays && !cfin);
+  int nact2;  // compact active list of the next beam, in beam order (row list source)
+  const int apos = block_prefix(stays && !cfin, wsm, &nact2);
+  if (stays && !cfin) st.c_act[base + apos] = act_pack(j - first, crow);
   if (tid == 0) {
     const int emitted = emitted0 + ne;
     st.slot_width[s] = width;
@@ -383,11 +416,9 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
 // and entry 2k+2 (the best excluded element) is a sentinel proving that no
 // excluded element can tie the 2k-th sum through fp64 merging of distinct
 // logps (flags InvariantViolation otherwise; needs |score| ~ 2^29 |dlogp|).
-__global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg, vs_state st, int M_rows) {
-  VS_PDL_ENTRY();
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_state& st, int M_rows,
+                                               unsigned char* smem) {
   const int b = blockIdx.x;
-  if (b >= st.status[VS_ST_NSEL]) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int k = cfg.k;
   const int s = st.sel[b];
@@ -466,12 +497,26 @@ __global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg,
         pt[b0 + q + 1] = tv;
       }
     if (has_sent) {  // boundary proof against the best excluded element
-      const int64_t ri = (int64_t)(row0 + a) * M_rows + Mi;
-      const float lsent = st.top_logp[ri];
-      const int tsent = st.top_tok[ri];
+      const int64_t rb = (int64_t)(row0 + a) * M_rows;
+      const float lsent = st.top_logp[rb + Mi];
+      const int tsent = st.top_tok[rb + Mi];
       const double ssent = sc + (double)lsent;
       const int bT = b0 + Mu - 1;  // the parent's 2k-th entry by sum
-      if (ssent == ps[bT] && (pl[bT] != lsent || tsent < pt[bT])) s_err = 1;
+      if (ssent == ps[bT] && lsent != -INFINITY) {
+        // the sentinel ties the 2k-th sum: it (and the excluded elements tied
+        // with it, which have larger tokens) must sort after it, and no excluded
+        // element with a smaller logp may round onto the same fp64 sum.  fp64
+        // addition is monotone, so the first listed logp below the sentinel's
+        // (K1 returns a few slack entries past it) bounds all of them.
+        bool bad = tsent < pt[bT];
+        if (!bad) {
+          int q = Mi + 1;
+          while (q < M_rows && st.top_logp[rb + q] == lsent) ++q;
+          if (q < M_rows) bad = sc + (double)st.top_logp[rb + q] == ssent;
+          else bad = M_rows < V;  // all slack entries tie the sentinel and more exist
+        }
+        if (bad) s_err = 1;
+      }
     }
   }
   __syncthreads();
@@ -620,13 +665,15 @@ __global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg,
     st.c_row[base + krank] = crow;
     st.c_fin[base + krank] = (uint8_t)cfin;
     if (src >= 0 && !cfin) {
-      const int slot = atomicAdd(st.n_copy, 1);
+      const int slot = atomicAdd(&st.counters[4], 1);  // published as *n_copy by the last CTA
       st.copy_list[3 * slot + 0] = base + src;
       st.copy_list[3 * slot + 1] = base + crow;
       st.copy_list[3 * slot + 2] = L;
     }
   }
-  const int nact2 = __syncthreads_count(stays && !cfin);
+  int nact2;  // compact active list of the next beam, in beam order (row list source)
+  const int apos = block_prefix(stays && !cfin, wsm, &nact2);
+  if (stays && !cfin) st.c_act[base + apos] = act_pack(krank, crow);
   if (tid == 0) {
     const int emitted = emitted0 + ne;
     st.slot_width[s] = width;
@@ -638,44 +685,116 @@ __global__ void __launch_bounds__(NT2) beam_step_immediate_kernel(vs_config cfg,
     if (finished) st.slot_flags[s] |= 2;
   }
 }
+
+// One CTA per slot (grid = n; CTAs past the selection only count in).  The last
+// CTA to finish publishes the step's copy count (*n_copy) and, with `sched`,
+// runs the scheduler for the next step (removal, refill, selection, row list),
+// so K2 and K3 are one launch.
+template <bool IMM>
+__global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows, int sched, int N,
+                                                        int admit_mode, int select_mode, int32_t* mirror) {
+  VS_PDL_ENTRY();
+  VS_PROF_T0(blockIdx.x == 0);
+  extern __shared__ __align__(16) unsigned char smem[];
+  if ((int)blockIdx.x < st.status[VS_ST_NSEL]) {
+    if (IMM) beam_immediate(cfg, st, M_rows, smem);
+    else beam_deferred(cfg, st, M_rows, smem);
+  }
+  __syncthreads();
+  VS_PROF(blockIdx.x == 0, 7);
+  // Grid completion: every other CTA signals its arrival; CTA 0 (always the
+  // same CTA, so the scheduler's code stays warm in one SM's instruction
+  // cache from step to step) waits for them, publishes the step's copy count
+  // and runs the scheduler.  No deadlock: CTA 0 only waits after its own work
+  // and occupies one slot while the others run on the remaining ones.
+  if (blockIdx.x != 0) {
+    if (threadIdx.x == 0) {
+      __threadfence();  // this CTA's state writes before its arrival
+      atomicAdd(&st.counters[5], 1);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const int want = (int)gridDim.x - 1;
+    while (true) {
+      int got;
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(&st.counters[5]) : "memory");
+      if (got >= want) break;
+      __nanosleep(32);
+    }
+    st.counters[5] = 0;
+    *st.n_copy = atomicExch(&st.counters[4], 0);
+    __threadfence();
+  }
+  __syncthreads();
+  VS_PROF(true, 8);
+  if (sched)
+    schedule_block<NT2>(cfg, st, N, 0, 1, admit_mode, select_mode, mirror, reinterpret_cast<int*>(smem));
+  VS_PROF(true, 15);
+  VS_PROF_FLUSH(true);
+}
+
 }  // namespace
+int32_t* mapped_ptr(void* host);
 }  // namespace vs
 
+static int launch_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_rows, int sched, int32_t N,
+                            int32_t admit_mode, int32_t select_mode, int32_t* status_mirror, void* stream);
+
 extern "C" int vs_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_rows, void* stream) {
+  return launch_beam_step(cfg, st, M_rows, 0, 0, VS_ADMIT_NONE, VS_SELECT_MIN_LT, nullptr, stream);
+}
+
+extern "C" int vs_beam_step_schedule(const vs_config* cfg, const vs_state* st, int32_t M_rows, int32_t N,
+                                     int32_t admit_mode, int32_t select_mode, int32_t* status_mirror,
+                                     void* stream) {
+  if (!cfg || cfg->n < 1 || cfg->n > VS_MAX_SLOTS || N < 1 || cfg->capacity < cfg->k) return VS_ERR_CONFIG;
+  return launch_beam_step(cfg, st, M_rows, 1, N, admit_mode, select_mode, status_mirror, stream);
+}
+
+static int launch_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_rows, int sched, int32_t N,
+                            int32_t admit_mode, int32_t select_mode, int32_t* status_mirror, void* stream) {
   if (!cfg || !st || cfg->k < 1 || cfg->k > VS_MAX_K || cfg->max_candidates < 1 ||
       cfg->max_candidates > cfg->k || M_rows < 1)
     return VS_ERR_CONFIG;
   const int k = cfg->k;
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
-  if (cfg->policy == VS_POLICY_IMMEDIATE) {
+  int32_t* mirror = vs::mapped_ptr(status_mirror);
+  if (status_mirror && !mirror) return VS_ERR_CONFIG;
+  const bool imm = cfg->policy == VS_POLICY_IMMEDIATE;
+  size_t smem;
+  if (imm) {
     const int Mi = min(2 * k + 1, cfg->vocab_size);
     if (M_rows < min(2 * k + 2, cfg->vocab_size) || 2 * k > vs::NT2) return VS_ERR_CONFIG;
     const int Pmax = k * Mi;
-    const size_t smem = (size_t)2 * k * 8 + (size_t)Pmax * (8 + 4 + 4 + 4) + (size_t)14 * k * 4 + 64;
-    if (smem > 200 * 1024) return VS_ERR_CONFIG;
-    static size_t configured_i = 0;
-    if (smem > 48 * 1024 && smem > configured_i) {
-      if (cudaFuncSetAttribute(vs::beam_step_immediate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return VS_ERR_CUDA;
-      configured_i = smem;
-    }
-    vs::vs_launch(vs::beam_step_immediate_kernel, dim3(cfg->n), dim3(vs::NT2), smem, strm, *cfg, *st, M_rows);
-    VS_CUDA_RET();
+    smem = (size_t)2 * k * 8 + (size_t)Pmax * (8 + 4 + 4 + 4) + (size_t)14 * k * 4 + 64;
+  } else {
+    if (cfg->policy != VS_POLICY_DEFERRED) return VS_ERR_CONFIG;
+    const int Meff = cfg->max_candidates < cfg->vocab_size ? cfg->max_candidates : cfg->vocab_size;
+    if (M_rows < Meff) return VS_ERR_CONFIG;
+    const int Pmax = k + k * Meff;
+    smem = (size_t)(2 * k + Pmax) * 8 + (size_t)2 * Pmax * 4 + (size_t)15 * k * 4 + 64;
   }
-  if (cfg->policy != VS_POLICY_DEFERRED) return VS_ERR_CONFIG;
-  const int Meff = cfg->max_candidates < cfg->vocab_size ? cfg->max_candidates : cfg->vocab_size;
-  if (M_rows < Meff) return VS_ERR_CONFIG;
-  const int Pmax = k + k * Meff;
-  const size_t smem = (size_t)(2 * k + Pmax) * 8 + (size_t)2 * Pmax * 4 + (size_t)13 * k * 4 + 64;
+  if (sched) smem = std::max(smem, vs::sched_smem_bytes(cfg->n));
   if (smem > 200 * 1024) return VS_ERR_CONFIG;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    if (cudaFuncSetAttribute(vs::beam_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+  auto kern = imm ? vs::beam_step_kernel<true> : vs::beam_step_kernel<false>;
+  static size_t configured[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > configured[imm]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return VS_ERR_CUDA;
-    configured = smem;
+    configured[imm] = smem;
   }
-  vs::vs_launch(vs::beam_step_kernel, dim3(cfg->n), dim3(vs::NT2), smem, strm, *cfg, *st, M_rows);
+  vs::vs_launch(kern, dim3(cfg->n), dim3(vs::NT2), smem, strm, *cfg, *st, M_rows, sched, N, admit_mode,
+                select_mode, mirror);
   VS_CUDA_RET();
 }
+
+#ifdef VS_PHASE_PROF
+// Profiling builds: copy (and reset) the phase accumulators of the fused kernel.
+extern "C" int vs_debug_phase_times(unsigned long long* host32) {
+  cudaMemcpyFromSymbol(host32, g_prof_acc, 32 * sizeof(unsigned long long));
+  static unsigned long long zero[32] = {};
+  cudaMemcpyToSymbol(g_prof_acc, zero, sizeof(zero));
+  return 0;
+}
+#endif

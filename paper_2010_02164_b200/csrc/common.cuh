@@ -156,6 +156,32 @@ cudaError_t vs_launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 #define VS_PDL_ENTRY() ::vs::pdl_entry()
 
+// Phase timing probes (profiling builds only: -DVS_PHASE_PROF).  Thread 0
+// of the probing CTA keeps SM clock stamps in shared memory (no memory
+// traffic on the measured path); VS_PROF_FLUSH adds (stamp - start) per probe
+// to global accumulators once per launch.
+#ifdef VS_PHASE_PROF
+static __device__ unsigned long long g_prof_acc[32];
+static __shared__ long long s_prof[32];
+#define VS_PROF_T0(cond)                                     \
+  if ((cond) && threadIdx.x == 0) {                          \
+    for (int _q = 0; _q < 32; ++_q) s_prof[_q] = 0;          \
+    s_prof[0] = clock64();                                   \
+  }
+#define VS_PROF(cond, i) \
+  if ((cond) && threadIdx.x == 0) s_prof[i] = clock64()
+#define VS_PROF_FLUSH(cond)                                                        \
+  if ((cond) && threadIdx.x == 0) {                                                \
+    for (int _q = 1; _q < 31; ++_q)                                                \
+      if (s_prof[_q]) atomicAdd(&g_prof_acc[_q], (unsigned long long)(s_prof[_q] - s_prof[0])); \
+    atomicAdd(&g_prof_acc[31], 1ull);                                              \
+  }
+#else
+#define VS_PROF_T0(cond) (void)0
+#define VS_PROF(cond, i) (void)0
+#define VS_PROF_FLUSH(cond) (void)0
+#endif
+
 #define VS_CUDA_RET()                                              \
   do {                                                             \
     cudaError_t _e = cudaGetLastError();                           \

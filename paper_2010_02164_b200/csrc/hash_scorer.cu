@@ -57,6 +57,8 @@ template <>
 __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 
 // Persistent grid-stride over (row, 2048-column chunk) work items with the
+// live row count read from device memory; rows of freshly admitted beams
+// (length 1) hash their source inline (the encode, fused: one launch per step).
 // live row count read from device memory: no empty CTAs are launched for
 // rows beyond R_t.  8 consecutive tokens per thread, one 16-byte store (bf16).
 // Each thread writes HVPT 16-byte groups of 8 logits per (row, chunk) work item,
@@ -72,7 +74,20 @@ __global__ void __launch_bounds__(256) hash_logits_kernel(vs_config cfg, vs_stat
   for (int w = blockIdx.x; w < R * cols; w += gridDim.x) {
     const int r = w / cols, cchunk = w - r * cols;
     const int s = st.row_slot[r];
-    const uint64_t h = st.c_hash[s * cfg.k + st.row_cand[r]];
+    uint64_t h;
+    if (st.row_len[r] == 1) {  // a beam admitted by this step's schedule: encode it inline
+      const int input = st.slot_input[s];
+      uint64_t sh = mix64(hp.seed ^ 0x9E3779B97F4A7C15ull);  // == hash_encode_kernel
+      for (int p = st.src_off[input]; p < st.src_off[input + 1]; ++p)
+        sh = mix64(sh ^ ((uint64_t)st.src_tok[p] + 0x632BE59BD9B4E019ull));
+      h = prefix_init(sh, cfg.sos);
+      if (cchunk == 0 && threadIdx.x == 0) {  // the beam step extends c_hash
+        st.slot_seed[s] = sh;
+        st.c_hash[s * cfg.k] = h;
+      }
+    } else {
+      h = st.c_hash[s * cfg.k + st.row_cand[r]];
+    }
     const uint32_t key = (uint32_t)(h ^ (h >> 32));
     T* out = logits + (int64_t)r * ld;
 #pragma unroll

@@ -199,7 +199,7 @@ class TransformerScorer:
             self.copies += int(engine.t["n_copy"].item())
         N.check(engine.lib.vs_rows_copy(kv.data_ptr(), kv.stride(0) * es, kv.shape[0], kv.stride(1) * es,
                                         kv.stride(2) * es, engine.t["copy_list"].data_ptr(),
-                                        engine.t["n_copy"].data_ptr(), engine.capacity, engine.stream_ptr),
+                                        engine.t["n_copy"].data_ptr(), engine.max_copies, engine.stream_ptr),
                 "vs_rows_copy")
 
 
@@ -391,5 +391,5 @@ class GraphedTransformerScorer(TransformerScorer):
         es = kv.element_size()
         N.check(engine.lib.vs_rows_copy(kv.data_ptr(), kv.stride(0) * es, kv.shape[0], kv.stride(1) * es,
                                         kv.stride(2) * es, engine.t["copy_list"].data_ptr(),
-                                        engine.t["n_copy"].data_ptr(), engine.capacity, engine.stream_ptr),
+                                        engine.t["n_copy"].data_ptr(), engine.max_copies, engine.stream_ptr),
                 "vs_rows_copy")

@@ -106,11 +106,15 @@ class SearchEngine:
         k, n, L = config.k, config.n, config.max_len
         self.k, self.n, self.max_len = k, n, L
         self.capacity = min(config.capacity, n * k)  # a step can never need more rows
+        # a step plans at most one copy per surviving child: <= k per selected beam
+        self.max_copies = n * k
         immediate = config.policy is FinalizationPolicy.IMMEDIATE
         if immediate and 2 * config.k + 2 > N.VS_MAX_M:
             raise ConfigError(f"immediate policy needs 2k+2 <= {N.VS_MAX_M}")
         # immediate ranks each parent's top-(2k+1) by sum, + 1 sentinel (bb/search.py:159-166)
-        self.m_rows = m_rows or (min(2 * config.k + 2, vocab.size) if immediate
+        # + up to 6 slack entries that settle fp64 ties at the boundary (beam_step.cu)
+        slack = max(0, min(6, N.VS_MAX_M - (2 * config.k + 2)))
+        self.m_rows = m_rows or (min(2 * config.k + 2 + slack, vocab.size) if immediate
                                  else min(config.max_candidates, vocab.size))
         dev = self.device
         i32 = dict(dtype=torch.int32, device=dev)
@@ -129,8 +133,9 @@ class SearchEngine:
             "top_tok": z(self.capacity * self.m_rows, **i32),
             "top_logp": z(self.capacity * self.m_rows, dtype=torch.float32, device=dev),
             "row_lse": z(self.capacity, dtype=torch.float32, device=dev),
-            "copy_list": z(self.capacity * 3, **i32), "n_copy": z(1, **i32),
+            "copy_list": z(n * k * 3, **i32), "n_copy": z(1, **i32),
             "status": z(N.status_ints(n), **i32), "fallbacks": z(1, **i32),
+            "c_act": z(n * k, **i32),
         }
         self.status_host = torch.zeros(N.status_ints(n), dtype=torch.int32, pin_memory=True)
         self.cfg = N.VsConfig(k=k, n=n, max_candidates=config.max_candidates, max_len=L,
@@ -148,7 +153,7 @@ class SearchEngine:
         self._hdr = None   # pinned status ring of the sync-free driver
         self._bufs = {}    # grow-only corpus / output buffers
         self._forks = {}   # scorer forks bound to this engine (concurrent batches)
-        self._graphs, self._graph_key = None, None
+        self._graphs, self._graph_key, self._graph_scorer = None, None, None
 
     # ------------------------------------------------------------------ data
     @property
@@ -230,9 +235,11 @@ class SearchEngine:
                              host["tok"].numpy().copy(), k, L, tok_off=off)
 
     # --------------------------------------------------------------- kernels
-    def schedule(self, *, first: bool, remove: bool, admit: int, select: int) -> None:
-        N.check(self.lib.vs_schedule(C.byref(self.cfg), C.byref(self.state), self.N, int(first),
-                                     int(remove), admit, select, self.stream_ptr), "vs_schedule")
+    def schedule(self, *, first: bool, remove: bool, admit: int, select: int, mirror: int | None = None) -> None:
+        """Standalone K3 (first schedule of a run, flush transitions)."""
+        N.check(self.lib.vs_schedule_mirror(C.byref(self.cfg), C.byref(self.state), self.N, int(first),
+                                            int(remove), admit, select, mirror, self.stream_ptr),
+                "vs_schedule_mirror")
 
     def read_status(self) -> np.ndarray:
         self.status_host.copy_(self.t["status"], non_blocking=True)
@@ -261,23 +268,35 @@ class SearchEngine:
         N.check(self.lib.vs_beam_step(C.byref(self.cfg), C.byref(self.state), self.m_rows,
                                       self.stream_ptr), "vs_beam_step")
 
+    def beam_step_schedule(self, *, admit: int, select: int, mirror: int | None = None) -> None:
+        """K2 with K3 fused into its last CTA: this step's prune/finalise plus
+        the next step's removal, refill, selection and row list."""
+        N.check(self.lib.vs_beam_step_schedule(C.byref(self.cfg), C.byref(self.state), self.m_rows, self.N,
+                                               admit, select, mirror, self.stream_ptr),
+                "vs_beam_step_schedule")
+
     def status_ptr(self, idx: int) -> int:
         return self.t["status"].data_ptr() + 4 * idx
 
     # ---------------------------------------------------------------- drivers
-    def _step(self, scorer, st: np.ndarray, *, phase: str) -> None:
+    def _step(self, scorer, st: np.ndarray, *, phase: str, admit: int, select: int) -> None:
+        """One timestep: scorer, K1, then K2 with the NEXT step's schedule
+        (modes admit/select) fused into its last CTA, then the scorer's K4."""
         R = int(st[N.ST_R])
-        if phase == "stream" and st[N.ST_NADMIT] > 0:
+        if st[N.ST_NADMIT] > 0:
             scorer.on_admit(self, st)
         logits, code = scorer.logits(self, R)
         if code != N.VS_K1_DONE:
             self.row_topm(logits, code, R, R)
-        self.beam_step()
+        self.beam_step_schedule(admit=admit, select=select)
         scorer.after_step(self, R)
 
     def run(self, corpus, scorer, *, admit_mode: int, select_mode: int, flush_enabled: bool,
             trace: bool = False, on_step: Callable | None = None):
-        """Synchronous driver mirroring bb/scheduler.py:243-287 step for step."""
+        """Synchronous driver mirroring bb/scheduler.py:243-287 step for step.
+        The schedule that opens iteration t+1 (removal of step t's finished
+        beams, flush check, refill, selection) runs inside step t's fused
+        beam-step launch, so the host decides its modes before launching."""
         cfgd = self.config
         self.load_corpus(corpus)
         scorer.bind(self)
@@ -287,7 +306,8 @@ class SearchEngine:
         timestep = 0
         next_flush = cfgd.flush_interval if flush_enabled and cfgd.flush_interval else None
         pending = None  # event fields of the last executed step, awaiting removal info
-        removed, first = True, True
+        FLUSH = (N.VS_ADMIT_NONE, N.VS_SELECT_ALL)
+        STREAM = (admit_mode, select_mode)
 
         def close_event(st):
             nonlocal pending
@@ -298,54 +318,66 @@ class SearchEngine:
                 on_step(StepEvent(*pending, fin, live))
             pending = None
 
-        def execute(st, phase, refilled):
+        def execute(st, phase, refilled, nxt):
             nonlocal timestep, pending
-            self._step(scorer, st, phase=phase)
+            self._step(scorer, st, phase=phase, admit=nxt[0], select=nxt[1])
             timestep += 1
             R, L = int(st[N.ST_R]), int(st[N.ST_L])
             report.record_step(R, L, cost)
             sel = tuple(int(x) for x in st[N.ST_HDR:N.ST_HDR + st[N.ST_NSEL]])
             pending = (timestep, phase, refilled, sel, R, L)
+            st2 = self.read_status()
+            close_event(st2)
+            return st2
 
+        # the first iteration's top (bb/scheduler.py:261-270); flush_interval >= 1
+        phase = "stream"
+        self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode)
+        st = self.read_status()
         while True:
-            if next_flush is not None and timestep >= next_flush:  # bb/scheduler.py:262-265
-                self.schedule(first=first, remove=not removed, admit=N.VS_ADMIT_NONE,
-                              select=N.VS_SELECT_ALL)
-                first, removed = False, True
-                st = self.read_status()
-                close_event(st)
-                while st[N.ST_NLIVE] > 0:
-                    execute(st, "flush", ())
-                    self.schedule(first=False, remove=True, admit=N.VS_ADMIT_NONE,
-                                  select=N.VS_SELECT_ALL)
-                    st = self.read_status()
-                    close_event(st)
+            if phase == "flush":  # bb/scheduler.py:262-265 flush_all: drain every live beam
+                if st[N.ST_NLIVE] > 0:
+                    st = execute(st, "flush", (), FLUSH)
+                    continue
                 next_flush = timestep + cfgd.flush_interval
-            self.schedule(first=first, remove=not removed, admit=admit_mode, select=select_mode)
-            first, removed = False, True
-            st = self.read_status()
-            close_event(st)
+                phase = "stream"
+                self.schedule(first=False, remove=False, admit=admit_mode, select=select_mode)
+                st = self.read_status()
             if st[N.ST_NLIVE] == 0:
                 break
             a0, na = int(st[N.ST_ADMIT0]), int(st[N.ST_NADMIT])
-            execute(st, "stream", tuple(range(a0, a0 + na)))
-            removed = False
+            flush_next = next_flush is not None and timestep + 1 >= next_flush
+            st = execute(st, "stream", tuple(range(a0, a0 + na)), FLUSH if flush_next else STREAM)
+            phase = "flush" if flush_next else "stream"
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
         return self.results(), report
 
-    def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 8,
-                    trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None):
+    def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 16,
+                    trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None,
+                    steps_per_graph: int = 4):
         """Generator form of the host-sync-free driver: every ``next()``
-        launches one step (on the CUDA stream current at that call) and
-        consumes the status snapshot ``ring`` steps behind; it returns the
+        launches a few steps (on the CUDA stream current at that call) and
+        consumes status snapshots ``ring`` steps behind; it returns the
         MetricsReport (StopIteration.value).  Several engines' generators can
-        be interleaved on separate streams (``drive_concurrent``)."""
+        be interleaved on separate streams (``drive_concurrent``).
+
+        Step l runs the scorer, K1 and the fused beam-step kernel, whose last
+        CTA schedules step l+1 and writes that status header straight into
+        pinned slot hdr[(l+1) % ring] (no copy launch).  With a graph-safe
+        scorer, ``steps_per_graph`` consecutive steps are one CUDA graph
+        replay (programmatic dependent launch chains every kernel, across
+        steps too); the device keeps stepping past the end of the stream
+        with empty steps until the host sees the final snapshot."""
         cfgd = self.config
         self.load_corpus(corpus, src_tok=src_tok, src_off=src_off)
         scorer.bind(self)
         report = MetricsReport.new(trace=trace)
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
+        graphed = getattr(scorer, "graph_safe", False) and k1_events is None
+        spg = max(1, steps_per_graph) if graphed else 1
+        ring = max(ring, 2 * spg)
+        ring += (-ring) % spg  # a multiple of spg: graph g always writes the same slots
         if self._hdr is None or self._hdr.shape[0] != ring:
             self._hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
         hdr = self._hdr
@@ -353,46 +385,46 @@ class SearchEngine:
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)
         launched = processed = 0
-        # one CUDA graph per ring slot replays the whole step (status snapshot,
-        # scorer, K1, K2, K3) when the scorer only launches device work
-        graphs = None
-        if getattr(scorer, "graph_safe", False) and k1_events is None:
-            graphs = self._step_graphs(scorer, ring, admit_mode, select_mode)
-        self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode)
-        while True:
-            slot = launched % ring
-            if launched - processed >= ring:  # consume the oldest snapshot
+        graphs = self._step_graphs(scorer, ring, spg, admit_mode, select_mode) if graphed else None
+        stream = torch.cuda.current_stream(self.device)
+        self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode, mirror=hdr[0].data_ptr())
+        events[0].record(stream)
+        done = False
+        while not done:
+            # launching steps launched..launched+spg-1 overwrites snapshot slots
+            # up to launched+spg: everything older than that must be consumed
+            while launched + spg - processed >= ring:
                 events[processed % ring].synchronize()
                 st = hdr[processed % ring].numpy()
                 if st[N.ST_ERROR]:
                     self.read_status()
                 if st[N.ST_NLIVE] == 0:
+                    done = True
                     break
                 report.record_step(int(st[N.ST_R]), int(st[N.ST_L]), cost)
                 processed += 1
+            if done:
+                break
             stream = torch.cuda.current_stream(self.device)
             if graphs is not None:
-                graphs[slot].replay()
-                events[slot].record(stream)
-                launched += 1
-                yield
-                continue
-            hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
-            events[slot].record(stream)
-            scorer.on_admit(self, None)
-            logits, code = scorer.logits(self, None)
-            if k1_events is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            if code != N.VS_K1_DONE:
-                self.row_topm(logits, code, 0, cap, d_R)
-            if k1_events is not None:
-                e1.record(stream)
-                k1_events.append((e0, e1))
-            self.beam_step()
-            scorer.after_step(self, None)
-            self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
-            launched += 1
+                graphs[(launched // spg) % len(graphs)].replay()
+            else:
+                scorer.on_admit(self, None)
+                logits, code = scorer.logits(self, None)
+                if k1_events is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                if code != N.VS_K1_DONE:
+                    self.row_topm(logits, code, 0, cap, d_R)
+                if k1_events is not None:
+                    e1.record(stream)
+                    k1_events.append((e0, e1))
+                self.beam_step_schedule(admit=admit_mode, select=select_mode,
+                                        mirror=hdr[(launched + 1) % ring].data_ptr())
+                scorer.after_step(self, None)
+            for q in range(1, spg + 1):
+                events[(launched + q) % ring].record(stream)
+            launched += spg
             yield
         self.launched_steps = launched
         st = self.read_status()
@@ -400,12 +432,18 @@ class SearchEngine:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
         return report
 
-    def _step_graphs(self, scorer, ring: int, admit_mode: int, select_mode: int):
-        """Capture (once per engine state / scorer binding) one graph per ring
-        slot: status snapshot -> pinned slot, scorer launches, K1, K2, K3."""
-        key = (id(scorer), ring, admit_mode, select_mode, self.N,  # N is a K3 launch argument
+    def _step_graphs(self, scorer, ring: int, spg: int, admit_mode: int, select_mode: int):
+        """Capture (once per engine state / scorer binding) ring/spg graphs of
+        spg steps each: scorer launches, K1, K2+K3 (status header -> the next
+        pinned slot)."""
+        # the graphs bake in the scorer's parameters and buffer addresses: key on
+        # the scorer object itself (held strongly, compared with `is`, so a
+        # recycled id() can never match) plus its graph_key() (parameters and
+        # data pointers, which change when bind() reallocates)
+        gk = scorer.graph_key() if hasattr(scorer, "graph_key") else None
+        key = (gk, ring, spg, admit_mode, select_mode, self.N,  # N is a K3 launch argument
                tuple(getattr(self.state, f) for f in N.STATE_FIELDS), self._hdr.data_ptr())
-        if self._graph_key == key:
+        if self._graph_key == key and self._graph_scorer is scorer:
             return self._graphs
         cap, d_R = self.capacity, self.status_ptr(N.ST_R)
         nbytes = int(self.lib.vs_row_lse_topm_ws_bytes(cap, self.vocab.size, N.VS_DTYPE_F32))
@@ -413,23 +451,24 @@ class SearchEngine:
             self._k1_ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         torch.cuda.current_stream(self.device).synchronize()
         graphs = []
-        for slot in range(ring):
+        for gi in range(ring // spg):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                self._hdr[slot].copy_(self.t["status"][: N.ST_HDR], non_blocking=True)
-                scorer.on_admit(self, None)
-                logits, code = scorer.logits(self, None)
-                if code != N.VS_K1_DONE:
-                    self.row_topm(logits, code, 0, cap, d_R)
-                self.beam_step()
-                scorer.after_step(self, None)
-                self.schedule(first=False, remove=True, admit=admit_mode, select=select_mode)
+                for q in range(spg):
+                    step = gi * spg + q
+                    scorer.on_admit(self, None)
+                    logits, code = scorer.logits(self, None)
+                    if code != N.VS_K1_DONE:
+                        self.row_topm(logits, code, 0, cap, d_R)
+                    self.beam_step_schedule(admit=admit_mode, select=select_mode,
+                                            mirror=self._hdr[(step + 1) % ring].data_ptr())
+                    scorer.after_step(self, None)
             graphs.append(g)
-        self._graphs, self._graph_key = graphs, key
+        self._graphs, self._graph_key, self._graph_scorer = graphs, key, scorer
         return graphs
 
     def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
-                  ring: int = 8, trace: bool = False, src_tok=None, src_off=None,
+                  ring: int = 16, trace: bool = False, src_tok=None, src_off=None,
                   materialize: bool = True, k1_events: list | None = None):
         """Host-sync-free driver (no flush / no StepEvents): every kernel reads
         R_t from device memory, status headers are streamed into a pinned ring

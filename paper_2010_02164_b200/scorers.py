@@ -67,6 +67,10 @@ class DeviceHashScorer:
     def signature(self) -> tuple:
         return ("hash", self.vocab.size, self.seed, self.scale, self.power, self.eos_bias, self.dtype)
 
+    def graph_key(self) -> tuple:
+        """What a captured step graph bakes in: parameters and buffer address."""
+        return self.signature + (self._buf.data_ptr() if self._buf is not None else 0,)
+
     def fork(self) -> "DeviceHashScorer":
         """An identical scorer for another engine (concurrent batches)."""
         return DeviceHashScorer(self.vocab, self.seed, scale=self.scale, power=self.power,
@@ -82,9 +86,7 @@ class DeviceHashScorer:
                                      eos_bias=self.eos_bias, power=self.power, dtype=self.code)
 
     def on_admit(self, engine, status) -> None:
-        N.check(engine.lib.vs_hash_encode(C.byref(engine.cfg), C.byref(engine.state),
-                                          C.c_uint64(self.seed & ((1 << 64) - 1)),
-                                          engine.stream_ptr), "vs_hash_encode")
+        pass  # the logits kernel encodes admitted sources inline (rows of length 1)
 
     def logits(self, engine, R):
         grid = engine.capacity if R is None else R

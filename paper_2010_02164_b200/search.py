@@ -154,6 +154,8 @@ def expand_beam(beam: Beam, score_rows, config: DecodeConfig, vocab: Vocabulary,
         eng.row_topm(rows, N.VS_DTYPE_F32 | N.VS_ROWS_NORMALIZED, nact, nact)
     eng.beam_step()
     t = eng.t
+    if int(t["counters"][3]):  # device-detected contract break (bb/search.py:155-158 etc.)
+        raise InvariantViolation(f"beam step error {int(t['counters'][3])}")
     k, L = eng.k, eng.max_len
     width = int(t["slot_width"][0])
     emitted_total = int(t["slot_emitted"][0])
