@@ -42,6 +42,7 @@ extern "C" {
 
 #define VS_DTYPE_F32 0
 #define VS_DTYPE_BF16 1
+#define VS_DTYPE_F64 2 /* normalised fp64 log-prob rows only (vs_row_topm_f64) */
 /* OR-ed into dtype: rows are already log-probs (reference Scorer rows,
  * bb/model.py:86); lse is taken as 0 so logp = fp32(row). */
 #define VS_ROWS_NORMALIZED 0x100
@@ -95,6 +96,10 @@ typedef struct vs_config {
 #define VS_ST_ERROR 8       /* 0 or VS_ERR_*                                */
 #define VS_ST_NFIN 9        /* beams removed as finished (previous step)    */
 #define VS_ST_NLIVE_AFTER 10 /* live count right after removal               */
+#define VS_ST_TOKFILL 11    /* tokens appended to out_tok so far this run   */
+#define VS_ST_MINLIVE 12    /* every input below this id is finished: its
+                               outputs (and their tokens, all below
+                               TOKFILL) are final                           */
 #define VS_ST_HDR 16
 /* followed by: selected input ids [n], finished input ids [n],
  * live-after-removal input ids [n], admitted slot ids [n]  (total HDR+4n). */
@@ -126,7 +131,8 @@ typedef struct vs_state {
   /* scheduler */
   int32_t* live;         /* [n] slot ids in arrival order               */
   int32_t* counters;     /* [8]: n_live, cursor, N, error, copy counter,
-                            CTA arrival counter (zero-initialised)      */
+                            CTA arrival counter, out_tok fill
+                            (zero-initialised)                          */
   int32_t* sel;          /* [n] selected slot ids, in advance order     */
   int32_t* sel_off;      /* [n+1] row offsets of selected beams         */
   int32_t* row_slot;     /* [capacity] slot of each scored row          */
@@ -140,7 +146,8 @@ typedef struct vs_state {
   int32_t* out_count;    /* [N]                                         */
   int32_t* out_len;      /* [N*k]                                       */
   double* out_score;     /* [N*k]                                       */
-  int32_t* out_tok;      /* [N*k*max_len]                               */
+  int32_t* out_tok;      /* append buffer (capacity N*k*max_len): the
+                            emitted candidates' tokens back to back     */
   /* per-row top-M (written by the row kernel) [capacity*M] */
   int32_t* top_tok;
   float* top_logp;
@@ -154,6 +161,12 @@ typedef struct vs_state {
    * (cand | phys_row << 8), written by the beam step and by admission; the
    * scheduler builds the next row list from it */
   int32_t* c_act;
+  /* [capacity*M] fp64 row values of the top-M entries, or NULL.  Set when the
+   * rows are reference fp64 log-probs (vs_row_topm_f64): the beam step then
+   * adds these exact values instead of the fp32 top_logp (bb/search.py:71). */
+  double* top_logp64;
+  /* [N*k] start of each emitted candidate's tokens in out_tok */
+  int32_t* out_off;
 } vs_state;
 
 /* Library identification / sanity. */
@@ -171,6 +184,16 @@ int vs_version(void);
 int vs_row_lse_topm(const void* logits, int32_t dtype, int64_t ld, int32_t V, int32_t M,
                     int32_t R_host, const int32_t* d_R, int32_t R_grid, int32_t* top_tok,
                     float* top_logp, float* row_lse, int32_t* fallback_count, void* stream);
+
+/* K1-f64 — per-row top-M over NORMALISED fp64 log-prob rows (the rows a
+ * reference Scorer returns, bb/model.py:86, :216-217): top-M tokens by
+ * (row value desc, token asc) (bb/search.py:69), the exact fp64 values into
+ * top_logp64 (and, if non-NULL, their fp32 roundings into top_logp).  NaN
+ * entries never rank; V < M pads with token -1 / -inf.  Parity path for host
+ * scorers: one warp per row, M arg-max rounds. */
+int vs_row_topm_f64(const double* rows, int64_t ld, int32_t V, int32_t M, int32_t R_host,
+                    const int32_t* d_R, int32_t R_grid, int32_t* top_tok, float* top_logp,
+                    double* top_logp64, void* stream);
 
 /* K1 with a caller-provided workspace — same contract and outputs as
  * vs_row_lse_topm.  When the rows qualify (16-byte aligned logits and

@@ -246,17 +246,18 @@ class TorchDecoderCPU:
 
     def __init__(self, vocab_size: int, sos: int, eos: int, *, d: int = 1024, heads: int = 16,
                  layers: int = 6, enc_layers: int = 6, ffn: int = 4096, seed: int = 0, tau: float = 6.0,
-                 eos_bias: float = 20.0):
+                 eos_bias: float = 20.0, weights: str = "bf16"):
         import torch
 
         self.torch = torch
         self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
         self.d, self.h, self.tau, self.eos_bias = d, heads, tau, eos_bias
         g = torch.Generator(device="cpu").manual_seed(seed)
+        rnd = (lambda t: t.to(torch.bfloat16).float()) if weights == "bf16" else (lambda t: t)
 
         def w(*shape, std=None):  # same draw order / scaling as decoder.TransformerScorer
             std = std if std is not None else 1.0 / math.sqrt(shape[-1])
-            return (torch.randn(*shape, generator=g) * std).to(torch.bfloat16).float()
+            return rnd(torch.randn(*shape, generator=g) * std)
 
         V = vocab_size
         self.emb = w(V, d, std=1.0)
@@ -264,8 +265,12 @@ class TorchDecoderCPU:
         self.enc = [dict(qkv=w(3 * d, d), o=w(d, d), f1=w(ffn, d), f2=w(d, ffn)) for _ in range(enc_layers)]
         self.dec = [dict(qkv=w(3 * d, d), o=w(d, d), cq=w(d, d), ckv=w(2 * d, d), co=w(d, d),
                          f1=w(ffn, d), f2=w(d, ffn)) for _ in range(layers)]
-        out = (torch.randn(V, d, generator=g) * (1.0 / math.sqrt(d))).to(torch.bfloat16)
-        self.out_s = (out.float() * tau).to(torch.bfloat16).float()  # tau folded, as on the device
+        out = torch.randn(V, d, generator=g) * (1.0 / math.sqrt(d))
+        if weights == "bf16":  # tau folded into the bf16 weight, as GraphedTransformerScorer does
+            self.out_s = (out.to(torch.bfloat16).float() * tau).to(torch.bfloat16).float()
+            self.post_tau = 1.0
+        else:  # fp32 TransformerScorer: tau * (h @ W_out^T)
+            self.out_s, self.post_tau = out, tau
 
     def _attn(self, q, k, v, mask):
         F = self.torch.nn.functional
@@ -310,7 +315,8 @@ class TorchDecoderCPU:
                 x = F.layer_norm(x + self._attn(q, k, v, causal) @ L["o"].T, (self.d,))
                 x = F.layer_norm(x + self._attn(x @ L["cq"].T, ck, cv, None) @ L["co"].T, (self.d,))
                 x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (self.d,))
-            lg = (x[0, -1] @ self.out_s.T).double()
+            lg = (x[0, -1] @ self.out_s.T)
+            lg = (lg * self.post_tau if self.post_tau != 1.0 else lg).double()
         lg[self.eos] += self.eos_bias * T / enc.input_len
         peak = float(lg.max())
         return (lg - (peak + math.log(float(torch.exp(lg - peak).sum())))).numpy()

@@ -15,13 +15,22 @@ from .metrics import CostParams, MetricsReport, StepRecord, round_half_up, step_
 __version__ = "0.1.0"
 
 _LAZY = {
-    "SearchEngine": "engine", "StepEvent": "engine", "DecodeResults": "engine",
+    "SearchEngine": "engine", "StepEvent": "engine", "Harvest": "engine",
     "refill_threshold": "engine",
     "DeviceHashScorer": "scorers", "HostScorerAdapter": "scorers", "BatchedScorer": "scorers",
     "run_varstream": "scheduler", "run_varbeam": "scheduler", "run_varfifo": "scheduler",
     "run_greedy": "scheduler",
     "dispatch_engine": "scheduler", "ENGINES": "scheduler",
-    "expand_beam": "search", "row_lse_topm": "search",
+    "expand_beam": "search", "expand_beams": "search", "row_lse_topm": "search",
+    "beam_finished": "api", "advance_beam": "api", "beam_decode": "api", "greedy_decode": "api",
+    "HeuristicConfig": "api", "max_candidates_filter": "api", "absolute_threshold_filter": "api",
+    "apply_heuristics": "api", "BeamSlot": "api", "BatchState": "api", "StepSelection": "api",
+    "refill": "api", "select_min_lt": "api", "select_fifo_max_lt": "api", "flush_all": "api",
+    "execute_step": "api",
+    "Corpus": "harness", "SyntheticCorpusSpec": "harness", "ExperimentConfig": "harness",
+    "run_experiment": "harness", "ResultsDocument": "harness", "load_corpus": "harness",
+    "save_corpus": "harness", "bucket_by_length": "harness", "generate_synthetic_corpus": "harness",
+    "build_scorer": "harness",
 }
 
 

@@ -16,7 +16,7 @@ from .errors import ConfigError, InvariantViolation
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libvarstream.so"
 
 VS_OK, VS_ERR_CONFIG, VS_ERR_INVARIANT, VS_ERR_CUDA = 0, -1, -3, -4
-VS_DTYPE_F32, VS_DTYPE_BF16, VS_ROWS_NORMALIZED = 0, 1, 0x100
+VS_DTYPE_F32, VS_DTYPE_BF16, VS_DTYPE_F64, VS_ROWS_NORMALIZED = 0, 1, 2, 0x100
 VS_K1_SPLIT, VS_K1_WARP = 0x200, 0x400  # pin the K1 kernel (vs_row_lse_topm_ws)
 # BatchedScorer.logits may return this code: the scorer already produced K1's
 # outputs (top_tok / top_logp / row_lse) for the step, e.g. with the fused K5 head
@@ -27,7 +27,7 @@ VS_SELECT_MIN_LT, VS_SELECT_FIFO, VS_SELECT_ALL = 0, 1, 2
 VS_MAX_K, VS_MAX_M, VS_MAX_SLOTS = 128, 128, 1024
 
 ST_R, ST_NSEL, ST_NLIVE, ST_L, ST_NADMIT, ST_ADMIT0, ST_CURSOR, ST_DONE = range(8)
-ST_ERROR, ST_NFIN, ST_NLIVE_AFTER = 8, 9, 10
+ST_ERROR, ST_NFIN, ST_NLIVE_AFTER, ST_TOKFILL, ST_MINLIVE = 8, 9, 10, 11, 12
 ST_HDR = 16
 
 
@@ -48,7 +48,7 @@ STATE_FIELDS = [
     "slot_flags", "slot_seed", "c_score", "c_len", "c_row", "c_fin", "c_hash", "hist", "live",
     "counters", "sel", "sel_off", "row_slot", "row_cand", "row_phys", "row_len", "src_off",
     "src_tok", "out_count", "out_len", "out_score", "out_tok", "top_tok", "top_logp", "row_lse",
-    "copy_list", "n_copy", "status", "c_act",
+    "copy_list", "n_copy", "status", "c_act", "top_logp64", "out_off",
 ]
 
 
@@ -65,7 +65,7 @@ class VsHashParams(C.Structure):
 EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step",
            "vs_beam_step_schedule", "vs_schedule", "vs_schedule_mirror", "vs_rows_copy",
            "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention", "vs_row_attention_grouped",
-           "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes")
+           "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes", "vs_row_topm_f64")
 
 _lib = None
 
@@ -86,6 +86,7 @@ def load_library(path: Path | None = None) -> C.CDLL:
         "vs_row_lse_topm_ws": ([vp, i32, i64, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, C.c_size_t, vp],
                                i32),
         "vs_row_lse_topm_ws_bytes": ([i32, i32, i32], C.c_size_t),
+        "vs_row_topm_f64": ([vp, i64, i32, i32, i32, vp, i32, vp, vp, vp, vp], i32),
         "vs_beam_step": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, vp], i32),
         "vs_schedule": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp], i32),
         "vs_schedule_mirror": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp, vp], i32),

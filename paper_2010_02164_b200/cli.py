@@ -8,8 +8,10 @@ Same flags and JSON-config merge as the reference; exit codes 0 success,
 (bb/cli.py:154-162).  Model files (JSON "kind"):
   device_hash  -> DeviceHashScorer (seed, scale, power, eos_bias, dtype)
   transformer  -> TransformerScorer (seed, d, heads, layers, enc_layers, ffn, max_src, tau, eos_bias)
-  seeded_hash / ngram_table -> the reference's own scorer (requires `beambatch`
-                  importable), run through HostScorerAdapter; search on device.
+  lstm         -> LSTMScorer (seed, emb, hidden, tau, eos_bias)
+The reference's seeded_hash / ngram_table scorers are out of scope (SURVEY.md
+§2.1): exit code 2.  Reference Scorer objects plug in through the Python API
+(run_experiment(ExperimentConfig(..., scorer_spec=<scorer>)), HostScorerAdapter).
 """
 
 from __future__ import annotations
@@ -69,36 +71,6 @@ def _delta(v):
     return float(v)
 
 
-def build_scorer(model: dict):
-    try:
-        kind = model["kind"]
-        vocab = Vocabulary(int(model["vocab_size"]), int(model["sos"]), int(model["eos"]))
-    except KeyError as exc:
-        raise DataError(f"model file missing field {exc}") from exc
-    if kind == "device_hash":
-        from .scorers import DeviceHashScorer
-
-        return DeviceHashScorer(vocab, int(model.get("seed", 0)), scale=float(model.get("scale", 0.5)),
-                                power=int(model.get("power", 0)), eos_bias=float(model.get("eos_bias", 4.0)),
-                                dtype=str(model.get("dtype", "bf16")))
-    if kind == "transformer":
-        from .decoder import TransformerScorer
-
-        keys = ("d", "heads", "layers", "enc_layers", "ffn", "max_src", "seed")
-        kw = {k: int(model[k]) for k in keys if k in model}
-        for k in ("tau", "eos_bias"):
-            if k in model:
-                kw[k] = float(model[k])
-        return TransformerScorer(vocab, **kw)
-    if kind in ("seeded_hash", "ngram_table"):
-        try:
-            from beambatch import ScorerSpec  # the reference's own model
-        except ImportError as exc:
-            raise DataError(f"model kind {kind!r} needs the reference package `beambatch`") from exc
-        return ScorerSpec.from_dict(model).build()
-    raise DataError(f"unknown model kind {kind!r}")
-
-
 def main(argv=None) -> int:
     try:
         args = _parser().parse_args(argv)
@@ -132,23 +104,22 @@ def main(argv=None) -> int:
                 model = json.loads(Path(model).read_text())
             except json.JSONDecodeError as exc:
                 raise DataError(f"model file is not valid JSON: {exc}") from exc
-        scorer = build_scorer(model)
         corpus = args.corpus or file_cfg.get("corpus")
         seed = args.seed if args.seed is not None else int(file_cfg.get("seed", 0))
         trace = args.trace if args.trace is not None else bool(file_cfg.get("trace", False))
         out = args.out or file_cfg.get("out")
-        from .harness import load_corpus, run_experiment
+        from .harness import ExperimentConfig, SyntheticCorpusSpec, run_experiment
 
         if isinstance(corpus, dict):
             if "synthetic" not in corpus:
                 raise ConfigError("corpus object form must contain a 'synthetic' block")
-            doc = run_experiment(engine, scorer, decode, synthetic=corpus["synthetic"], out_path=out,
-                                 trace=trace, seed=seed, model_echo=model)
+            exp = ExperimentConfig(engine, model, decode, synthetic=SyntheticCorpusSpec.from_dict(corpus["synthetic"]),
+                                   out_path=out, trace=trace, seed=seed)
         elif corpus is not None:
-            doc = run_experiment(engine, scorer, decode, corpus=load_corpus(corpus), out_path=out,
-                                 trace=trace, seed=seed, model_echo=model)
+            exp = ExperimentConfig(engine, model, decode, corpus_path=corpus, out_path=out, trace=trace, seed=seed)
         else:
             raise ConfigError("a corpus is required (--corpus or config file)")
+        doc = run_experiment(exp)
     except ConfigError as exc:
         print(f"config error: {exc}", file=sys.stderr)
         return 1

@@ -38,6 +38,12 @@ namespace {
 constexpr int NT2 = 128;  // == VS_MAX_K: one thread per candidate / child
 constexpr unsigned FULLM = 0xffffffffu;
 
+// Row value of top-M entry i: the exact fp64 row value when the rows were
+// reference fp64 log-probs (vs_row_topm_f64), else K1's fp32 logp.
+__device__ __forceinline__ double row_logp(const vs_state& st, int64_t i) {
+  return st.top_logp64 ? st.top_logp64[i] : (double)st.top_logp[i];
+}
+
 struct Pool {
   const double* sc;
   const int* par;
@@ -66,6 +72,28 @@ __device__ __forceinline__ int block_prefix(bool pred, int* wsm, int* total) {
   __syncthreads();
   *total = tot;
   return off + __popc(b & ((1u << lane) - 1u));
+}
+
+// Block-wide (NT2 threads) exclusive prefix sum of v.
+__device__ __forceinline__ int block_prefix_sum(int v, int* wsm, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULLM, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsm[wid] = x;
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < NT2 / 32; ++q) {
+    off += q < wid ? wsm[q] : 0;
+    tot += wsm[q];
+  }
+  __syncthreads();
+  *total = tot;
+  return off + x - v;
 }
 
 __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_state& st, int M_rows,
@@ -101,8 +129,9 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
   int* nlen = csrc + k;                               // [k] child length
   int* ctok = nlen + k;                               // [k] child's new token (-1: no-op)
   int* prow = ctok + k;                               // [k] row holding the child's prefix
+  int* eoff = prow + k;                               // [k] emission q's start in out_tok
   __shared__ int wsm[NT2 / 32];
-  __shared__ int s_kept, s_nextra;
+  __shared__ int s_kept, s_nextra, s_ebase;
   __shared__ double s_cut;
 
   // ---- candidates -> smem; stable finalized / active split ---------------------
@@ -143,7 +172,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
       const int a = (e - nfz) / Meff, m = (e - nfz) - a * Meff;
       const int i = act[a];
       const int64_t ri = (int64_t)(row0 + a) * M_rows + m;
-      ps[e] = cs[i] + (double)st.top_logp[ri];  // fp64 add, bb/search.py:71
+      ps[e] = cs[i] + row_logp(st, ri);  // fp64 add, bb/search.py:71
       pp[e] = i;
       pt[e] = st.top_tok[ri];
     }
@@ -328,6 +357,15 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     }
   }
   __syncthreads();
+  // emissions append their tokens to out_tok: one atomic per beam reserves them
+  {
+    int etot;
+    const int epre = block_prefix_sum(j < ne ? nlen[emo[j]] : 0, wsm, &etot);
+    if (tid == 0 && etot > 0) s_ebase = atomicAdd(&st.counters[6], etot);
+    __syncthreads();
+    if (j < ne) eoff[j] = s_ebase + epre;
+    __syncthreads();
+  }
   VS_PROF(blockIdx.x == 0, 5);
   // ---- token histories + emission, one flattened phase ---------------------------
   // Every read is of a claimed row's prefix [0, L) (a parent's, or a no-op's own
@@ -343,6 +381,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     const int64_t o = (int64_t)input * k + emitted0 + j;
     st.out_len[o] = nlen[c];
     st.out_score[o] = ps[kept[c]];
+    st.out_off[o] = eoff[j];
   }
   {
     const int T1 = nextra * L, T = T1 + ne * (L + 1);
@@ -363,7 +402,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
           if (p < nlen[c]) {
             const bool last = ctok[c] >= 0 && p == nlen[c] - 1;
             val[u] = last ? ctok[c] : st.hist[(int64_t)(base + prow[c]) * ML + p];
-            dst[u] = st.out_tok + ((int64_t)input * k + emitted0 + q) * ML + p;
+            dst[u] = st.out_tok + (int64_t)eoff[q] + p;
           }
         }
       }
@@ -472,8 +511,8 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
     bool sorted = true;
     for (int m = 0; m < Mi; ++m) {
       const int64_t ri = (int64_t)(row0 + a) * M_rows + m;
-      const float lp = st.top_logp[ri];
-      pl[b0 + m] = lp;
+      const double lp = row_logp(st, ri);
+      pl[b0 + m] = (float)lp;
       pt[b0 + m] = st.top_tok[ri];
       pp[b0 + m] = a;
       ps[b0 + m] = sc + (double)lp;  // bb/search.py:163
@@ -498,9 +537,9 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
       }
     if (has_sent) {  // boundary proof against the best excluded element
       const int64_t rb = (int64_t)(row0 + a) * M_rows;
-      const float lsent = st.top_logp[rb + Mi];
+      const double lsent = row_logp(st, rb + Mi);
       const int tsent = st.top_tok[rb + Mi];
-      const double ssent = sc + (double)lsent;
+      const double ssent = sc + lsent;
       const int bT = b0 + Mu - 1;  // the parent's 2k-th entry by sum
       if (ssent == ps[bT] && lsent != -INFINITY) {
         // the sentinel ties the 2k-th sum: it (and the excluded elements tied
@@ -511,8 +550,8 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
         bool bad = tsent < pt[bT];
         if (!bad) {
           int q = Mi + 1;
-          while (q < M_rows && st.top_logp[rb + q] == lsent) ++q;
-          if (q < M_rows) bad = sc + (double)st.top_logp[rb + q] == ssent;
+          while (q < M_rows && row_logp(st, rb + q) == lsent) ++q;
+          if (q < M_rows) bad = sc + row_logp(st, rb + q) == ssent;
           else bad = M_rows < V;  // all slack entries tie the sentinel and more exist
         }
         if (bad) s_err = 1;
@@ -611,6 +650,14 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
   }
   __syncthreads();
   const int ML = cfg.max_len;
+  // every emission of this step (EOS proposals, then the length-cap drain) has
+  // L + 1 tokens: one atomic reserves them all in the out_tok append buffer
+  const bool drain = !cfg.no_drain && L + 1 >= cfg.max_len && nkept > 0;
+  const int nd = drain ? min(k - emitted0 - n_emit, nkept) : 0;
+  __shared__ int s_ebase;
+  if (tid == 0 && n_emit + nd > 0) s_ebase = atomicAdd(&st.counters[6], (n_emit + nd) * (L + 1));
+  __syncthreads();
+  const int ebase = s_ebase;
   // ---- EOS emissions straight from the parent's row + eos (warp per emission) -------
   const int input = st.slot_input[s];
   for (int q = wid; q < kk; q += NT2 / 32) {
@@ -621,12 +668,14 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
     for (int q2 = 0; q2 < q; ++q2) er += pt[scan[q2]] == cfg.eos;
     if (er >= quota) continue;
     const int64_t o = (int64_t)input * k + emitted0 + er;
+    const int64_t to = (int64_t)ebase + (int64_t)er * (L + 1);
     const int32_t* srcp = st.hist + (int64_t)(base + cr[pp[e]]) * ML;
-    for (int p = lane; p < L; p += 32) st.out_tok[o * ML + p] = srcp[p];
+    for (int p = lane; p < L; p += 32) st.out_tok[to + p] = srcp[p];
     if (lane == 0) {
-      st.out_tok[o * ML + L] = cfg.eos;
+      st.out_tok[to + L] = cfg.eos;
       st.out_len[o] = L + 1;
       st.out_score[o] = ps[e];
+      st.out_off[o] = (int32_t)to;
     }
   }
   __syncthreads();  // parents' rows are read above before free rows are overwritten
@@ -642,14 +691,16 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
   __syncthreads();
   // ---- length-cap drain of the kept fill (all cap-finalised) --------------------------
   int width = nkept, ne = n_emit;
-  if (!cfg.no_drain && L + 1 >= cfg.max_len && nkept > 0) {
-    const int q2 = k - emitted0 - n_emit;
-    const int nd = min(q2, nkept);
+  if (drain) {
     for (int c = wid; c < nd; c += NT2 / 32) {
       const int64_t o = (int64_t)input * k + emitted0 + n_emit + c;
+      const int64_t to = (int64_t)ebase + (int64_t)(n_emit + c) * (L + 1);
       const int32_t* srcp = st.hist + (int64_t)(base + nrow[c]) * ML;
-      for (int p = lane; p <= L; p += 32) st.out_tok[o * ML + p] = srcp[p];
-      if (lane == 0) st.out_len[o] = L + 1;
+      for (int p = lane; p <= L; p += 32) st.out_tok[to + p] = srcp[p];
+      if (lane == 0) {
+        st.out_len[o] = L + 1;
+        st.out_off[o] = (int32_t)to;
+      }
     }
     // scores of drained children
     if (kept && krank < nd) st.out_score[(int64_t)input * k + emitted0 + n_emit + krank] = csc;
@@ -773,7 +824,7 @@ static int launch_beam_step(const vs_config* cfg, const vs_state* st, int32_t M_
     const int Meff = cfg->max_candidates < cfg->vocab_size ? cfg->max_candidates : cfg->vocab_size;
     if (M_rows < Meff) return VS_ERR_CONFIG;
     const int Pmax = k + k * Meff;
-    smem = (size_t)(2 * k + Pmax) * 8 + (size_t)2 * Pmax * 4 + (size_t)15 * k * 4 + 64;
+    smem = (size_t)(2 * k + Pmax) * 8 + (size_t)2 * Pmax * 4 + (size_t)16 * k * 4 + 64;
   }
   if (sched) smem = std::max(smem, vs::sched_smem_bytes(cfg->n));
   if (smem > 200 * 1024) return VS_ERR_CONFIG;

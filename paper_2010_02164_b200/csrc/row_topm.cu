@@ -32,6 +32,7 @@ namespace vs {
 namespace {
 
 constexpr int WPC = 8;                 // warps per CTA (W warps per row, WPC/W rows)
+constexpr int NSEG = WPC;              // fixed lse segments per row (any W divides it)
 constexpr int CAPW = 416;              // per-warp candidate buffer (keys)
 constexpr int FLUSH_MIN = 16;
 #ifndef PICKW_C0
@@ -394,8 +395,10 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   __shared__ uint64_t ssel[WPC][VS_MAX_M];
   __shared__ unsigned shist[WPC][256];
   __shared__ PartSmem spart[WPC];
+  __shared__ float2 segp[WPC][NSEG + 1];  // per row (at its leader): segment (m, s) pairs
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int R = d_R ? *d_R : R_host;
+  if ((int)blockIdx.x >= R) return;  // idle for any W (a CTA starts at row >= blockIdx.x)
   const int W = pick_w(R, V, sms * warps_per_sm, c0);
   const int part = wid % W, leader = wid - part;
   const int r = blockIdx.x * (WPC / W) + wid / W;
@@ -417,6 +420,26 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   const unsigned long long L2E2 = pk2(VS_LOG2E, VS_LOG2E);
   Cand c{0ull, -INFINITY, 0};
   TopList<K> tl{(K)0, (K)0, -INFINITY};
+  // one warp vote per vector guards both rare paths: gate = min(θx, m_thr)
+  float gate = fminf(TL ? tl.theta_x : c.theta_x, m_thr);
+  // Partition-invariant lse: the row is cut into NSEG fixed segments (plus the
+  // scalar tail as segment NSEG); each segment's (m, s) pair starts from a fresh
+  // m and is streamed with the same lane mapping whichever warp owns it, and the
+  // row's lse is the in-order left fold of the NSEG+1 pairs.  So lse (and every
+  // logp) of a row is bit-identical whatever W the live row count picks.
+  auto seg_flush = [&](int idx) {
+    float a, b;
+    up2(s01, a, b);
+    float sv = a + b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(FULL, sv, o);
+    if (lane == 0) segp[wid - wid % W][idx] = make_float2(m, sv);
+    m = M_FLOOR;
+    m_thr = M_FLOOR + RESCALE_MARGIN;
+    nml2 = pk2(-M_FLOOR * VS_LOG2E, -M_FLOOR * VS_LOG2E);
+    s01 = pk2(0.0f, 0.0f);
+    gate = fminf(TL ? tl.theta_x : c.theta_x, m_thr);
+  };
 
   // Candidate path of one vector (warp-synchronous).
   auto cand = [&](const float (&x)[VEC], int n, int tok0) {
@@ -443,7 +466,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     for (int j = 1; j < VEC; ++j) cm = fmaxf(cm, x[j]);
     // One warp vote guards both rare paths: θx <= (warp max so far) <= m_thr, so
     // an element above m_thr also passes the candidate test.
-    if (__any_sync(FULL, cm >= (TL ? tl.theta_x : c.theta_x))) {
+    if (__any_sync(FULL, cm >= gate)) {
       if (__any_sync(FULL, cm > m_thr)) {  // raise the shared max, rescale the sums
         float mw = cm;
 #pragma unroll
@@ -454,7 +477,8 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         m_thr = m + RESCALE_MARGIN;
         nml2 = pk2(-m * VS_LOG2E, -m * VS_LOG2E);
       }
-      cand(x, n, tok0);
+      if (__any_sync(FULL, cm >= (TL ? tl.theta_x : c.theta_x))) cand(x, n, tok0);
+      gate = fminf(TL ? tl.theta_x : c.theta_x, m_thr);
     }
 #pragma unroll
     for (int j = 0; j < VEC; j += 2) {
@@ -491,11 +515,8 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         c.theta_x = t0;
       }
     }
-    if (m0 > M_FLOOR) {
-      m = m0;
-      m_thr = m0 + RESCALE_MARGIN;
-      nml2 = pk2(-m * VS_LOG2E, -m * VS_LOG2E);
-    }
+    (void)m0;  // the running max is per segment (partition-invariant lse)
+    gate = fminf(TL ? tl.theta_x : c.theta_x, m_thr);
   };
   // lane max with its first token over one vector (bootstrap only)
   auto lane_argmax = [&](const float (&x)[VEC], int tok0, float& lm, int& lt) {
@@ -510,8 +531,12 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   if (active) {
     const bool vec_ok = (reinterpret_cast<uintptr_t>(row) & 15) == 0;
     const int ntot = vec_ok ? V / VEC : 0;
-    const int seg = (ntot + W - 1) / W;
-    const int v0 = min(ntot, part * seg), v1 = min(ntot, v0 + seg);
+    // NSEG segments of Qs vectors (a multiple of the double batch), NSEG/W per part
+    constexpr int DB = 2 * 32 * U;
+    const int Qs = ((ntot + NSEG - 1) / NSEG + DB - 1) / DB * DB;
+    const int spp = NSEG / W;
+    const int v0 = min(ntot, part * spp * Qs), v1 = min(ntot, v0 + spp * Qs);
+    int segi = part * spp, seg_next = v0 + Qs;
     const uint4* __restrict__ vrow = reinterpret_cast<const uint4*>(row);
     if constexpr (NS > 0) {
       constexpr int CH = 32 * U;  // vectors per chunk
@@ -552,6 +577,10 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         boot(lm, lt);
       }
       for (int ch = 0; ch < nch; ++ch) {
+        if (v0 + ch * CH == seg_next) {
+          seg_flush(segi++);
+          seg_next += Qs;
+        }
         const int q = ch % NS;
         tk::mbar_wait(&bars[q], (unsigned)(ch / NS) & 1u);
         const uint4* sv = stg + q * CH;
@@ -622,6 +651,10 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
       }
       // full double-batches: no per-vector bounds checks
       for (; base + 2 * BATCH <= v1; base += 2 * BATCH) {
+        if (base == seg_next) {
+          seg_flush(segi++);
+          seg_next += Qs;
+        }
         if (lane == 0 && pf_batches > 0) {
           const int p0 = base + pf_dist, p1 = min(v1, p0 + 2 * BATCH);
           if (p1 > p0) l2_prefetch(vrow + p0, (unsigned)(p1 - p0) * 16u);
@@ -650,6 +683,10 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         }
       }
       // remainder (< 2 batches, already loaded into cur / nxt): checked
+      if (base == seg_next && base < v1) {
+        seg_flush(segi++);
+        seg_next += Qs;
+      }
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -665,7 +702,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         }
       }
     }
-    if (part == W - 1) {  // tail / unaligned rows
+    // close this part's segments (empty ones give (M_FLOOR, 0) pairs)
+    while (segi < (part + 1) * spp) seg_flush(segi++);
+    if (part == W - 1) {  // tail / unaligned rows: segment NSEG
       for (int i0 = ntot * VEC; i0 < V; i0 += 32) {
         const int i = i0 + lane;
         float x[VEC];
@@ -674,6 +713,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         for (int j = 1; j < VEC; ++j) x[j] = -INFINITY;
         consume(x, 1, i);
       }
+      seg_flush(NSEG);
     }
   }
   if (TL) {  // hand the list to the common epilogue as a sorted buffer
@@ -684,25 +724,20 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
     c.theta_x = tl.theta_x;
     __syncwarp();
   }
-  // ---- per-warp lse partial -> exchange --------------------------------------------
+  // ---- lse: in-order left fold of the row's segment pairs ----------------------------
+  // lane q holds pair q; the max and the rescaled sum are fixed xor trees over
+  // the same NSEG+1 pairs in every warp of the row (partition-invariant)
+  if (W > 1) __syncthreads();
+  else __syncwarp();
   float s;
   {
-    float a, b;
-    up2(s01, a, b);
-    s = a + b;
-  }
-  // m is warp-uniform (RESCALE_MARGIN), so the warp's partial sums add directly
+    const float2 pq = lane <= NSEG ? segp[leader][lane] : make_float2(-INFINITY, 0.0f);
+    m = pq.x;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-  if (W > 1) {
-    if (lane == 0) {
-      spart[wid].m = m;
-      spart[wid].s = s;
-    }
-    __syncthreads();
-    m = -INFINITY;
-    s = 0.0f;
-    for (int q = 0; q < W; ++q) lse_merge(m, s, spart[leader + q].m, spart[leader + q].s);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+    s = pq.y > 0.0f ? pq.y * ex2f((pq.x - m) * VS_LOG2E) : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
   }
   const float lse_raw = (m <= -1e30f || s == 0.0f) ? -INFINITY : m + logf(s);
   const float lse = normalized ? 0.0f : lse_raw;

@@ -316,6 +316,11 @@ __device__ void schedule_block(const vs_config& cfg, const vs_state& st, int N, 
       hdr[VS_ST_ERROR] = bad ? VS_ERR_CONFIG : sticky;
       hdr[VS_ST_NFIN] = nfin;
       hdr[VS_ST_NLIVE_AFTER] = n_live_after;
+      const int fill = first ? 0 : __ldcg(&st.counters[6]);
+      hdr[VS_ST_TOKFILL] = fill;
+      // arrival order == input order and removal is stable: live[0] is the
+      // oldest live input, and every input below it has finished
+      hdr[VS_ST_MINLIVE] = n_live > 0 ? input_s[live_s[0]] : cursor;
 #pragma unroll
       for (int q = 0; q < VS_ST_HDR; ++q) status[q] = hdr[q];
       // the host reads the mirror after an event recorded behind this kernel:
@@ -328,6 +333,7 @@ __device__ void schedule_block(const vs_config& cfg, const vs_state& st, int N, 
       st.counters[1] = cursor;
       st.counters[2] = N;
       st.counters[3] = sticky;
+      st.counters[6] = fill;
     }
   }
   __syncthreads();

@@ -24,7 +24,7 @@ import ctypes as C
 import itertools
 import math
 from dataclasses import dataclass
-from typing import Callable, Sequence
+from typing import Callable
 
 import numpy as np
 import torch
@@ -54,39 +54,84 @@ def refill_threshold(config: DecodeConfig) -> int:
     return math.floor(config.epsilon * config.n + 1e-9)
 
 
-class DecodeResults(Sequence):
-    """Per-input emitted candidates, in input order (bb/scheduler.py:287),
-    built lazily from the device outputs copied back to the host: per-input
-    counts, per-candidate lengths and scores, and the emitted tokens packed
-    back to back (``tok_off[o]`` = start of candidate slot ``o``)."""
+def _candidate(tokens, score, input_id, _new=object.__new__, _set=object.__setattr__, _C=Candidate):
+    """Candidate(tokens, score, True, input_id) without the frozen-dataclass
+    __init__ (the bulk materialisation of a decode's outputs)."""
+    c = _new(_C)
+    _set(c, "tokens", tokens)
+    _set(c, "score", score)
+    _set(c, "finalized", True)
+    _set(c, "input_id", input_id)
+    return c
 
-    def __init__(self, count, lens, scores, toks, k: int, max_len: int, tok_off=None):
-        self.count, self.lens, self.scores, self.toks = count, lens, scores, toks
-        self.k, self.max_len, self.tok_off = k, max_len, tok_off
 
-    def __len__(self) -> int:
-        return int(self.count.shape[0])
+class Harvest:
+    """Brings a decode's outputs to the host as ``list[list[Candidate]]``
+    (bb/scheduler.py:287) WHILE the device is still decoding.
 
-    def __getitem__(self, i):
-        if isinstance(i, slice):
-            return [self[j] for j in range(*i.indices(len(self)))]
-        if i < 0:
-            i += len(self)
-        out = []
-        for e in range(int(self.count[i])):
-            o = i * self.k + e
-            n = int(self.lens[o])
-            if self.tok_off is None:
-                toks = self.toks[o, :n]
-            else:
-                b = int(self.tok_off[o])
-                toks = self.toks[b:b + n]
-            out.append(Candidate(tuple(int(t) for t in toks), float(self.scores[o]), True, i))
-        return out
+    Emissions append their tokens to the ``out_tok`` buffer (one atomic per
+    beam, csrc/beam_step.cu), and every status snapshot carries the append
+    fill and MINLIVE, below which every input has finished (arrival order is
+    input order and removal is stable).  So whenever the sync-free driver
+    consumes a snapshot whose MINLIVE has advanced by ``chunk`` inputs, the
+    outputs of those inputs plus the tokens appended since the last request
+    are copied to pinned memory on the engine's stream (behind the kernels
+    that wrote them), and chunks whose copies have landed are turned into
+    Candidate lists — host work that overlaps the device's remaining steps.
+    The bytes moved are exactly the emitted outputs."""
 
-    @property
-    def d2h_bytes(self) -> int:
-        return int(self.count.nbytes + self.lens.nbytes + self.scores.nbytes + self.toks.nbytes)
+    def __init__(self, eng: "SearchEngine", out: list, gids=None, chunk: int = 256):
+        self.eng, self.out, self.gids, self.chunk = eng, out, gids, chunk
+        self.lo = 0          # inputs [0, lo) requested
+        self.tok_hi = 0      # out_tok[0, tok_hi) requested
+        self.toks: list = []  # host copy of out_tok[0, tok_hi), as Python ints
+        self.pending = []
+        self.d2h_bytes = 0
+
+    def offer(self, st) -> None:
+        """A status snapshot consumed by the driver (it is at most ring steps old)."""
+        hi = int(st[N.ST_MINLIVE])
+        if hi - self.lo >= self.chunk:
+            self._request(hi, int(st[N.ST_TOKFILL]))
+        self.poll()
+
+    def _request(self, hi: int, fill: int) -> None:
+        t, k, lo = self.eng.t, self.eng.k, self.lo
+        src = (t["out_count"][lo:hi], t["out_len"][lo * k:hi * k], t["out_score"][lo * k:hi * k],
+               t["out_off"][lo * k:hi * k], t["out_tok"][self.tok_hi:fill])
+        host = tuple(torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in src)
+        for h, x in zip(host, src):
+            h.copy_(x, non_blocking=True)
+            self.d2h_bytes += h.numel() * h.element_size()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.eng.device))
+        self.pending.append((ev, lo, hi, host))
+        self.lo, self.tok_hi = hi, fill
+
+    def poll(self, block: bool = False) -> None:
+        while self.pending and (block or self.pending[0][0].query()):
+            ev, lo, hi, host = self.pending.pop(0)
+            ev.synchronize()
+            count, lens, scores, offs, tok = host
+            self.toks.extend(tok.numpy().tolist())
+            self._materialize(lo, count.numpy().tolist(), lens.numpy().tolist(), scores.numpy().tolist(),
+                              offs.numpy().tolist())
+
+    def _materialize(self, lo, count, lens, scores, offs) -> None:
+        out, gids, toks, k = self.out, self.gids, self.toks, self.eng.k
+        for q, cnt in enumerate(count):
+            gi = lo + q if gids is None else int(gids[lo + q])
+            b = q * k
+            out[gi] = [_candidate(tuple(toks[offs[e]:offs[e] + lens[e]]), scores[e], gi)
+                       for e in range(b, b + cnt)]
+
+    def finish(self, st) -> list:
+        """After the run's final status (synchronised): request the rest, wait."""
+        fill = int(st[N.ST_TOKFILL])
+        if self.lo < self.eng.N or fill > self.tok_hi:
+            self._request(self.eng.N, fill)
+        self.poll(block=True)
+        return self.out
 
 
 class SearchEngine:
@@ -184,13 +229,17 @@ class SearchEngine:
         self.t["src_off"] = src_off if src_off.is_cuda else self._grow("src_off", src_off)
         self.t["src_tok"] = src_tok if src_tok.is_cuda else self._grow("src_tok", src_tok)
         k, L = self.k, self.max_len
+        if n_in * k * L >= 2 ** 31:
+            raise ConfigError(f"{n_in} inputs x k={k} x max_len={L} exceeds one engine's int32 token "
+                              "offsets; shard the corpus (streams / ranks)")
         for f, n, dt in (("out_count", n_in, torch.int32), ("out_len", n_in * k, torch.int32),
-                         ("out_score", n_in * k, torch.float64), ("out_tok", n_in * k * L, torch.int32)):
+                         ("out_score", n_in * k, torch.float64), ("out_off", n_in * k, torch.int32),
+                         ("out_tok", n_in * k * L, torch.int32)):
             buf = self._bufs.get(f)
             if buf is None or buf.numel() < n:  # only emitted entries are ever read
                 buf = self._bufs[f] = torch.empty(n, dtype=dt, device=dev)
             self.t[f] = buf[:n]
-        for f in ("src_off", "src_tok", "out_count", "out_len", "out_score", "out_tok"):
+        for f in ("src_off", "src_tok", "out_count", "out_len", "out_score", "out_off", "out_tok"):
             setattr(self.state, f, self.t[f].data_ptr())
 
     def _grow(self, name: str, src: torch.Tensor) -> torch.Tensor:
@@ -202,37 +251,32 @@ class SearchEngine:
         view.copy_(src, non_blocking=True)
         return view
 
-    def results(self) -> DecodeResults:
-        """Compact the emitted candidates on the device (counts, lengths,
-        scores, tokens packed back to back), then one D2H into reusable pinned
-        buffers: the bytes moved are those of the emitted outputs, not of the
-        [N, k, max_len] token buffer."""
-        k, L, n_in = self.k, self.max_len, self.N
-        t, dev = self.t, self.device
+    def results(self, out: list | None = None, gids=None) -> list:
+        """The run's outputs as list[list[Candidate]] in input order
+        (bb/scheduler.py:287): one D2H of the emitted outputs (the append
+        buffer's fill comes from the final status)."""
+        st = self.read_status().copy()
+        st[N.ST_TOKFILL] = int(self.t["counters"][6].item())  # authoritative fill (any driver)
+        h = Harvest(self, out if out is not None else [[] for _ in range(self.N)], gids, chunk=1 << 30)
+        res = h.finish(st)
+        self.last_d2h_bytes = h.d2h_bytes
+        return res
+
+    def packed(self):
+        """Emitted outputs packed in local input order, on the device:
+        (count [N] i32, lens [E] i32, scores [E] f64, tokens [T] i32) — what
+        the multi-GPU gather ships (parallel.gather_results)."""
+        t, k, n_in, dev = self.t, self.k, self.N, self.device
         count = t["out_count"][:n_in]
         emitted = (torch.arange(k, device=dev)[None, :] < count[:, None]).reshape(-1)
-        lens = torch.where(emitted, t["out_len"][: n_in * k].clamp(0, L), 0)  # slots never written stay harmless
+        lens = t["out_len"][: n_in * k][emitted]
+        scores = t["out_score"][: n_in * k][emitted]
+        offs = t["out_off"][: n_in * k][emitted].long()
         total = int(lens.sum().item())
-        slot = torch.repeat_interleave(torch.arange(n_in * k, device=dev), lens.long(), output_size=total)
-        starts = torch.cumsum(lens, 0, dtype=torch.int64) - lens
-        pos = torch.arange(total, device=dev) - starts[slot]
-        packed = t["out_tok"][: n_in * k * L].view(n_in * k, L)[slot, pos]
-        src = {"count": count, "lens": lens, "score": t["out_score"][: n_in * k], "tok": packed}
-        host = {}
-        for f, d in src.items():
-            buf = self._pinned.get(f)
-            if buf is None or buf.numel() < d.numel() or buf.dtype != d.dtype:
-                buf = torch.empty(max(d.numel(), 1), dtype=d.dtype, pin_memory=True)
-                self._pinned[f] = buf
-            host[f] = buf[: d.numel()]
-            host[f].copy_(d, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-        # the pinned staging buffers are reused by the next call: results own copies
-        lens_h = host["lens"].numpy().copy()
-        off = np.zeros(lens_h.shape[0], dtype=np.int64)
-        np.cumsum(lens_h[:-1], out=off[1:])
-        return DecodeResults(host["count"].numpy().copy(), lens_h, host["score"].numpy().copy(),
-                             host["tok"].numpy().copy(), k, L, tok_off=off)
+        seg = torch.repeat_interleave(torch.arange(lens.numel(), device=dev), lens.long(), output_size=total)
+        starts = torch.cumsum(lens.long(), 0) - lens.long()
+        idx = offs[seg] + (torch.arange(total, device=dev) - starts[seg])
+        return count.to(torch.int32), lens.to(torch.int32), scores, t["out_tok"][idx].to(torch.int32)
 
     # --------------------------------------------------------------- kernels
     def schedule(self, *, first: bool, remove: bool, admit: int, select: int, mirror: int | None = None) -> None:
@@ -254,6 +298,18 @@ class SearchEngine:
     def row_topm(self, logits: torch.Tensor, dtype_code: int, R_host: int, R_grid: int,
                  d_R: int | None = None) -> None:
         ld = logits.stride(0)
+        if dtype_code & 0xff == N.VS_DTYPE_F64:
+            # reference fp64 log-prob rows: exact values go to the beam step
+            if "top_logp64" not in self.t:
+                self.t["top_logp64"] = torch.zeros(self.capacity * self.m_rows, dtype=torch.float64,
+                                                   device=self.device)
+            self.state.top_logp64 = self.t["top_logp64"].data_ptr()
+            N.check(self.lib.vs_row_topm_f64(
+                logits.data_ptr(), ld, self.vocab.size, self.m_rows, R_host, d_R, R_grid,
+                self.t["top_tok"].data_ptr(), self.t["top_logp"].data_ptr(),
+                self.t["top_logp64"].data_ptr(), self.stream_ptr), "vs_row_topm_f64")
+            return
+        self.state.top_logp64 = None
         nbytes = int(self.lib.vs_row_lse_topm_ws_bytes(self.capacity, self.vocab.size, dtype_code))
         ws = self._k1_ws
         if ws is None or ws.numel() < nbytes:  # zeroed once; counters self-reset
@@ -288,6 +344,8 @@ class SearchEngine:
         logits, code = scorer.logits(self, R)
         if code != N.VS_K1_DONE:
             self.row_topm(logits, code, R, R)
+        else:
+            self.state.top_logp64 = None
         self.beam_step_schedule(admit=admit, select=select)
         scorer.after_step(self, R)
 
@@ -355,7 +413,7 @@ class SearchEngine:
 
     def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 16,
                     trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None,
-                    steps_per_graph: int = 4):
+                    steps_per_graph: int = 4, harvest_into: list | None = None, gids=None):
         """Generator form of the host-sync-free driver: every ``next()``
         launches a few steps (on the CUDA stream current at that call) and
         consumes status snapshots ``ring`` steps behind; it returns the
@@ -368,7 +426,11 @@ class SearchEngine:
         scorer, ``steps_per_graph`` consecutive steps are one CUDA graph
         replay (programmatic dependent launch chains every kernel, across
         steps too); the device keeps stepping past the end of the stream
-        with empty steps until the host sees the final snapshot."""
+        with empty steps until the host sees the final snapshot.
+
+        With ``harvest_into`` (a list indexed by global input id; ``gids`` maps
+        this engine's inputs to global ids) the outputs are streamed to the
+        host while the device decodes (``Harvest``)."""
         cfgd = self.config
         self.load_corpus(corpus, src_tok=src_tok, src_off=src_off)
         scorer.bind(self)
@@ -381,6 +443,7 @@ class SearchEngine:
         if self._hdr is None or self._hdr.shape[0] != ring:
             self._hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
         hdr = self._hdr
+        harvest = Harvest(self, harvest_into, gids) if harvest_into is not None else None
         events = [torch.cuda.Event() for _ in range(ring)]
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)
@@ -403,6 +466,8 @@ class SearchEngine:
                     break
                 report.record_step(int(st[N.ST_R]), int(st[N.ST_L]), cost)
                 processed += 1
+                if harvest is not None:
+                    harvest.offer(st)
             if done:
                 break
             stream = torch.cuda.current_stream(self.device)
@@ -430,6 +495,9 @@ class SearchEngine:
         st = self.read_status()
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
+        if harvest is not None:
+            harvest.finish(st)
+            self.last_d2h_bytes = harvest.d2h_bytes
         return report
 
     def _step_graphs(self, scorer, ring: int, spg: int, admit_mode: int, select_mode: int):
@@ -473,15 +541,18 @@ class SearchEngine:
         """Host-sync-free driver (no flush / no StepEvents): every kernel reads
         R_t from device memory, status headers are streamed into a pinned ring
         and consumed `ring` steps behind the device."""
+        n_in = len(corpus) if corpus is not None else int(src_off.shape[0]) - 1
+        out = [[] for _ in range(n_in)] if materialize else None
         gen = self.async_steps(corpus, scorer, admit_mode=admit_mode, select_mode=select_mode, ring=ring,
-                               trace=trace, src_tok=src_tok, src_off=src_off, k1_events=k1_events)
+                               trace=trace, src_tok=src_tok, src_off=src_off, k1_events=k1_events,
+                               harvest_into=out)
         while True:
             try:
                 next(gen)
             except StopIteration as stop:
                 report = stop.value
                 break
-        return (self.results() if materialize else None), report
+        return out, report
 
 
 def drive_concurrent(jobs):

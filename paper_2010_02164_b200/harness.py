@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import math
 import random
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -95,7 +96,7 @@ def load_corpus(path):
         inputs.append(toks)
     if not inputs:
         raise DataError(f"{path}: empty corpus")
-    return inputs
+    return Corpus(inputs)
 
 
 def save_corpus(corpus, path) -> None:
@@ -162,34 +163,128 @@ def decode_config_echo(config) -> dict:
             "cost_c1": config.cost_c1}
 
 
-def run_experiment(engine: str, scorer, decode, *, corpus=None, synthetic: dict | None = None,
-                   out_path=None, trace: bool = False, seed: int = 0, model_echo: dict | None = None):
-    """Load/synthesise the corpus, bucket by length, decode on the device with
-    `engine` (dispatch_engine), restore input order, optionally write results
-    and trace.  Returns a ResultsDocument."""
+class Corpus(tuple):
+    """bb/harness.py:35-44: ordered token-id inputs (``Corpus(inputs)``;
+    ``.inputs``, ``len``, indexing)."""
+
+    def __new__(cls, inputs=()):
+        return super().__new__(cls, (tuple(int(t) for t in x) for x in inputs))
+
+    @property
+    def inputs(self) -> tuple:
+        return tuple(self)
+
+
+@dataclass(frozen=True)
+class SyntheticCorpusSpec:
+    """bb/harness.py:118-138."""
+
+    n_inputs: int
+    distribution: str = "geometric"
+    mean_len: float = 8.0
+    min_len: int = 1
+    max_len: int = 16
+
+    @classmethod
+    def from_dict(cls, raw: dict) -> "SyntheticCorpusSpec":
+        try:
+            return cls(int(raw["n_inputs"]), str(raw.get("distribution", "geometric")),
+                       float(raw.get("mean_len", 8.0)), int(raw.get("min_len", 1)), int(raw.get("max_len", 16)))
+        except (KeyError, TypeError, ValueError) as exc:
+            raise ConfigError(f"bad synthetic corpus spec: {exc}") from exc
+
+
+def build_scorer(model: dict):
+    """A scorer from a model description (the CLI's model file): ``device_hash``
+    (csrc/hash_scorer.cu), ``transformer`` (decoder.TransformerScorer) or
+    ``lstm`` (decoder.LSTMScorer).  The reference's seeded-hash and n-gram
+    table scorers are out of scope; reference Scorer objects
+    plug in directly through the Python API (scorers.HostScorerAdapter)."""
+    from .core import Vocabulary
+
+    try:
+        kind = model["kind"]
+        vocab = Vocabulary(int(model["vocab_size"]), int(model["sos"]), int(model["eos"]))
+    except KeyError as exc:
+        raise DataError(f"model file missing field {exc}") from exc
+    if kind == "device_hash":
+        from .scorers import DeviceHashScorer
+
+        return DeviceHashScorer(vocab, int(model.get("seed", 0)), scale=float(model.get("scale", 0.5)),
+                                power=int(model.get("power", 0)), eos_bias=float(model.get("eos_bias", 4.0)),
+                                dtype=str(model.get("dtype", "bf16")))
+    if kind in ("transformer", "lstm"):
+        from . import decoder
+
+        keys = ("d", "heads", "layers", "enc_layers", "ffn", "max_src", "seed", "hidden", "emb")
+        kw = {k: int(model[k]) for k in keys if k in model}
+        for k in ("tau", "eos_bias"):
+            if k in model:
+                kw[k] = float(model[k])
+        cls = decoder.TransformerScorer if kind == "transformer" else decoder.LSTMScorer
+        return cls(vocab, **kw)
+    raise DataError(f"unknown model kind {kind!r} (this build: device_hash, transformer, lstm; "
+                    "the reference's seeded_hash / ngram_table scorers are out of scope)")
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """bb/harness.py:140-168.  ``scorer_spec`` is a model description dict
+    (``build_scorer``) or a scorer object (BatchedScorer or reference-protocol
+    Scorer)."""
+
+    engine: str
+    scorer_spec: object
+    decode: object
+    corpus_path: str | None = None
+    synthetic: SyntheticCorpusSpec | None = None
+    out_path: str | None = None
+    trace: bool = False
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        from .scheduler import ENGINES
+
+        if self.engine not in ENGINES:
+            raise ConfigError(f"unknown engine {self.engine!r}; expected one of {', '.join(ENGINES)}")
+        if (self.corpus_path is None) == (self.synthetic is None):
+            raise ConfigError("exactly one of corpus_path or synthetic is required")
+        if self.trace and self.out_path is None:
+            raise ConfigError("trace output requires an output path")
+        if self.engine in ("fixed", "fixedstream") and (
+                self.decode.delta != math.inf or self.decode.max_candidates != self.decode.k):
+            raise ConfigError(f"engine {self.engine!r} requires pruning off: delta=inf and max_candidates=k")
+
+
+def run_experiment(config: ExperimentConfig) -> ResultsDocument:
+    """bb/harness.py:280-331: load or synthesise the corpus, bucket by length,
+    decode on the device with the configured engine (dispatch_engine),
+    restore input order, optionally write the results and the trace."""
     from .scheduler import dispatch_engine
 
-    if (corpus is None) == (synthetic is None):
-        raise ConfigError("exactly one of corpus or synthetic is required")
-    if trace and out_path is None:
-        raise ConfigError("trace output requires an output path")
-    if synthetic is not None:
-        spec = dict(synthetic)
-        n_inputs = int(spec.pop("n_inputs"))
-        corpus = generate_synthetic_corpus(seed, n_inputs, scorer.vocab.size, **spec)
-        corpus_echo = {"synthetic": dict(synthetic) | {"seed": seed}}
+    spec = config.scorer_spec
+    scorer = build_scorer(spec) if isinstance(spec, dict) else spec
+    if config.corpus_path is not None:
+        corpus = load_corpus(config.corpus_path)
+        corpus_echo: dict = {"path": str(config.corpus_path)}
     else:
-        corpus_echo = {"inputs": len(corpus)}
+        syn = config.synthetic
+        corpus = generate_synthetic_corpus(config.seed, syn.n_inputs, scorer.vocab.size,
+                                           distribution=syn.distribution, mean_len=syn.mean_len,
+                                           min_len=syn.min_len, max_len=syn.max_len)
+        corpus_echo = {"synthetic": dict(syn.__dict__) | {"seed": config.seed}}
     bucketed, perm = bucket_by_length(corpus)
-    outputs, report = dispatch_engine(engine, bucketed, scorer, decode, trace=trace)
+    outputs, report = dispatch_engine(config.engine, bucketed, scorer, config.decode, trace=config.trace)
     records = [None] * len(corpus)
     for pos, orig in enumerate(perm):
         records[orig] = {"input_id": orig,
                          "candidates": [{"tokens": list(c.tokens), "score": c.score} for c in outputs[pos]]}
-    doc = ResultsDocument(engine, {"decode": decode_config_echo(decode), "model": model_echo or {},
-                                   "corpus": corpus_echo, "seed": seed}, report.summarize(), records)
-    if out_path is not None:
-        doc.write(out_path)
-        if trace:
-            write_trace(report, trace_path_for(out_path))
+    model_echo = spec if isinstance(spec, dict) else {"kind": type(spec).__name__}
+    doc = ResultsDocument(config.engine, {"decode": decode_config_echo(config.decode), "model": model_echo,
+                                          "corpus": corpus_echo, "seed": config.seed},
+                          report.summarize(), records)
+    if config.out_path is not None:
+        doc.write(config.out_path)
+        if config.trace:
+            write_trace(report, trace_path_for(config.out_path))
     return doc

@@ -11,28 +11,26 @@ lengths and fp64 scores, and the flat token stream.
 
 from __future__ import annotations
 
-from collections.abc import Sequence
-
 import numpy as np
 import torch
 import torch.distributed as dist
 
-from .core import Candidate
 from .harness import shard
 
 
-def pack_results(count: torch.Tensor, lens: torch.Tensor, scores: torch.Tensor, toks: torch.Tensor,
-                 k: int, max_len: int):
-    """Compact engine output buffers (device or CPU tensors) to the emitted
-    candidates only: (count [N] i32, lens [E] i32, scores [E] f64, flat tokens [T] i32)."""
+def pack_results(count: torch.Tensor, lens: torch.Tensor, scores: torch.Tensor, offs: torch.Tensor,
+                 toks: torch.Tensor, k: int):
+    """Compact engine output buffers (device or CPU tensors; the append layout
+    of include/varstream.h: count [n], lens / scores / offs [n*k], tokens
+    appended at offs) to the emitted candidates in input order:
+    (count [n] i32, lens [E] i32, scores [E] f64, flat tokens [T] i32)."""
     n = count.numel()
     dev = count.device
     emitted = (torch.arange(k, device=dev)[None, :] < count[:, None].long()).reshape(-1)
-    lens_e = lens.reshape(-1)[emitted].to(torch.int32)
-    scores_e = scores.reshape(-1)[emitted].to(torch.float64)
-    rows = toks.reshape(n * k, max_len)[emitted]
-    mask = torch.arange(max_len, device=dev)[None, :] < lens_e[:, None].long()
-    flat = rows[mask].to(torch.int32)
+    lens_e = lens.reshape(-1)[: n * k][emitted].to(torch.int32)
+    scores_e = scores.reshape(-1)[: n * k][emitted].to(torch.float64)
+    offs_e = offs.reshape(-1)[: n * k][emitted].long()
+    flat = toks.reshape(-1)[_ragged_index(offs_e, lens_e)].to(torch.int32)
     return count.to(torch.int32), lens_e, scores_e, flat
 
 
@@ -66,81 +64,91 @@ def merge_packs(packs, sub_ids, n_local: int):
     return count_l.to(torch.int32), lens_l.to(torch.int32), scores[cand], toks[tok].to(torch.int32)
 
 
-def _all_gather_ragged(t: torch.Tensor, group=None) -> list[torch.Tensor]:
+def serialize_pack(packed) -> torch.Tensor:
+    """One uint8 buffer per rank: 4 int64 sizes, then count | lens | tokens
+    (int32) and scores (fp64, 8-byte aligned) — a single message per rank."""
+    count, lens, scores, toks = packed
+    dev = count.device
+    sizes = torch.tensor([count.numel(), lens.numel(), toks.numel(), scores.numel()], dtype=torch.int64,
+                         device=dev)
+    parts = [sizes.view(torch.uint8), count.contiguous().view(torch.uint8), lens.contiguous().view(torch.uint8),
+             toks.contiguous().view(torch.uint8)]
+    ints = sum(p.numel() for p in parts[1:])
+    if ints % 8:
+        parts.append(torch.zeros(8 - ints % 8, dtype=torch.uint8, device=dev))
+    parts.append(scores.contiguous().view(torch.uint8))
+    return torch.cat(parts)
+
+
+def deserialize_pack(buf: np.ndarray):
+    """Inverse of serialize_pack on the host: (count, lens, scores, toks) numpy arrays."""
+    nc, nl, nt, ns = (int(x) for x in buf[:32].view(np.int64))
+    o = 32
+    count = buf[o:o + 4 * nc].view(np.int32)
+    o += 4 * nc
+    lens = buf[o:o + 4 * nl].view(np.int32)
+    o += 4 * nl
+    toks = buf[o:o + 4 * nt].view(np.int32)
+    o += 4 * nt
+    o += (-(o - 32)) % 8
+    scores = buf[o:o + 8 * ns].view(np.float64)
+    return count, lens, scores, toks
+
+
+def materialize(out: list, gids, count, lens, scores, toks) -> None:
+    """Candidate lists of a packed shard into `out` at global ids `gids`."""
+    from .engine import _candidate
+
+    tl, ll, sl = toks.tolist(), lens.tolist(), scores.tolist()
+    e = o = 0
+    for g, cnt in zip(np.asarray(gids).tolist(), count.tolist()):
+        per = []
+        for _ in range(cnt):
+            n_ = ll[e]
+            per.append(_candidate(tuple(tl[o:o + n_]), sl[e], g))
+            o += n_
+            e += 1
+        out[g] = per
+
+
+def gather_packed(packed, group=None, dst: int = 0):
+    """Ship every rank's packed results to rank `dst` as one self-describing
+    message per rank (its header holds the sizes): an all-reduce of the
+    message length, then one gather of the padded messages.  Returns the
+    per-rank uint8 buffers on `dst` (device-resident), None elsewhere."""
     world = dist.get_world_size(group)
-    size = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-    sizes = [torch.zeros_like(size) for _ in range(world)]
-    dist.all_gather(sizes, size, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    mx = max(max(sizes), 1)
-    pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
-    pad[: t.numel()] = t.reshape(-1)
-    bufs = [torch.empty(mx, dtype=t.dtype, device=t.device) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
-    return [b[:s] for b, s in zip(bufs, sizes)]
-
-
-class ShardedResults(Sequence):
-    """Global-order per-input candidate lists assembled on the gathering rank
-    (index arrays built with numpy: no per-input Python work up front)."""
-
-    def __init__(self, n_total: int, parts):
-        self.n = n_total
-        self.part = np.full(n_total, -1, dtype=np.int32)      # input -> part
-        self.cfirst = np.zeros(n_total, dtype=np.int64)       # input -> first candidate in its part
-        self.ccount = np.zeros(n_total, dtype=np.int64)
-        self.parts = []
-        for gids, count, lens, scores, toks in parts:
-            gids = np.asarray(gids, dtype=np.int64)
-            count = np.asarray(count, dtype=np.int64)
-            offs = np.zeros(len(lens) + 1, dtype=np.int64)
-            np.cumsum(lens, out=offs[1:])
-            cstart = np.zeros(len(count) + 1, dtype=np.int64)
-            np.cumsum(count, out=cstart[1:])
-            p = len(self.parts)
-            self.parts.append((lens, scores, toks, offs))
-            self.part[gids] = p
-            self.cfirst[gids] = cstart[:-1]
-            self.ccount[gids] = count
-
-    def __len__(self) -> int:
-        return self.n
-
-    def __getitem__(self, i):
-        if isinstance(i, slice):
-            return [self[j] for j in range(*i.indices(self.n))]
-        p, c0, cnt = int(self.part[i]), int(self.cfirst[i]), int(self.ccount[i])
-        lens, scores, toks, offs = self.parts[p]
-        return [Candidate(tuple(int(t) for t in toks[offs[c]:offs[c + 1]]), float(scores[c]), True, i)
-                for c in range(c0, c0 + cnt)]
-
-
-def gather_packed(packed, group=None):
-    """The one collective: all-gather every rank's packed (ragged) results;
-    returns, per field, the list of every rank's tensor (device-resident)."""
-    return [_all_gather_ragged(t, group) for t in packed]
+    rank = dist.get_rank(group)
+    msg = serialize_pack(packed)
+    mx = torch.tensor([msg.numel()], dtype=torch.int64, device=msg.device)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+    pad = torch.zeros(int(mx.item()), dtype=torch.uint8, device=msg.device)
+    pad[: msg.numel()] = msg
+    bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, bufs, dst=dst, group=group)
+    return bufs
 
 
 def gather_results(packed, n_total: int, group=None, dst: int = 0):
-    """All-gather every rank's packed results; rank `dst` returns
-    ShardedResults in global input order, the others return None."""
+    """The one data-plane exchange: every rank's packed
+    results travel as ONE message to rank `dst` (a gather of the message
+    sizes, then a gather of the size-padded messages — NCCL over NVLink on
+    B200, gloo in the CPU tests).  Rank `dst` returns list[list[Candidate]]
+    in global input order; the others return None."""
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    gathered = gather_packed(packed, group)
-    if rank != dst:
+    bufs = gather_packed(packed, group, dst)
+    if bufs is None:
         return None
-    parts = []
+    out = [[] for _ in range(n_total)]
     for r in range(world):
-        gids = shard(n_total, world, r)
-        count, lens, scores, toks = (g[r].cpu().numpy() for g in gathered)
-        parts.append((gids, count, lens, scores, toks))
-    return ShardedResults(n_total, parts)
+        host = bufs[r].cpu().numpy()
+        materialize(out, shard(n_total, world, r), *deserialize_pack(host))
+    return out
 
 
 def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0, streams: int = 1):
     """Public multi-GPU entry: this rank decodes its snake-dealt shard of the
     (length-sorted) corpus on its current CUDA device; outputs are gathered
-    to rank `dst`.  Returns (ShardedResults | None, local MetricsReport)."""
+    to rank `dst`.  Returns (list[list[Candidate]] | None, local MetricsReport)."""
     from . import _native as N
     from .engine import SearchEngine
     from .scheduler import _vocab
@@ -172,14 +180,12 @@ def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0, s
             rep.timesteps += r_.timesteps
             rep.candidate_expansions += r_.candidate_expansions
             rep.simulated_cost += r_.simulated_cost
-        packed = merge_packs([pack_results(e.t["out_count"], e.t["out_len"], e.t["out_score"], e.t["out_tok"],
-                                           e.k, e.max_len) for e in engs], subs, len(local))
+        packed = merge_packs([e.packed() for e in engs], subs, len(local))
     elif local:
         eng = SearchEngine(config, _vocab(scorer))
         _, rep = eng.run_async(local, scorer, admit_mode=N.VS_ADMIT_VARSTREAM,
                                select_mode=N.VS_SELECT_MIN_LT, materialize=False)
-        packed = pack_results(eng.t["out_count"], eng.t["out_len"], eng.t["out_score"],
-                              eng.t["out_tok"], eng.k, eng.max_len)
+        packed = eng.packed()
     else:  # more ranks than inputs
         from .metrics import MetricsReport
 

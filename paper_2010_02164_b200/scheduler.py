@@ -11,8 +11,6 @@ be a BatchedScorer (device) or any reference-protocol Scorer
 from __future__ import annotations
 
 import math
-from collections.abc import Sequence
-
 import torch
 
 from . import _native as N
@@ -36,30 +34,6 @@ def _as_batched(scorer, corpus):
 def _vocab(scorer) -> Vocabulary:
     v = scorer.vocab
     return v if isinstance(v, Vocabulary) else Vocabulary(v.size, v.sos, v.eos)
-
-
-class ConcurrentResults(Sequence):
-    """Global input order over the per-batch results of a concurrent run."""
-
-    def __init__(self, n: int, shards, parts):
-        self.where = [None] * n
-        for q, ids in enumerate(shards):
-            for li, g in enumerate(ids):
-                self.where[int(g)] = (q, li)
-        self.parts = parts
-
-    def __len__(self) -> int:
-        return len(self.where)
-
-    def __getitem__(self, i):
-        if isinstance(i, slice):
-            return [self[j] for j in range(*i.indices(len(self)))]
-        q, li = self.where[i]
-        return [Candidate(c.tokens, c.score, c.finalized, i) for c in self.parts[q][li]]
-
-    @property
-    def d2h_bytes(self) -> int:
-        return sum(p.d2h_bytes for p in self.parts)
 
 
 _ENGINES: dict = {}
@@ -93,19 +67,18 @@ def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
     is independent of batch composition (bb SPEC.md:379), so the candidates
     equal a single-batch run's; the MetricsReport sums the batches' counters."""
     shards = [shard(len(corpus), streams, q) for q in range(streams)]
+    out = [[] for _ in range(len(corpus))]
     engines, jobs = [], []
     for q in range(streams):
         eng, stream = _engine(config, _vocab(scorer), q)
         sc = scorer if q == 0 else _fork_for(eng, scorer)
         sub = [corpus[int(i)] for i in shards[q]]
-        gen = eng.async_steps(sub, sc, admit_mode=admit, select_mode=select, trace=trace)
+        # outputs stream into `out` (global ids) while the batches decode
+        gen = eng.async_steps(sub, sc, admit_mode=admit, select_mode=select, trace=trace,
+                              harvest_into=out, gids=shards[q])
         engines.append(eng)
         jobs.append((stream, gen))
     reports = drive_concurrent(jobs)
-    parts = []
-    for eng, (stream, _) in zip(engines, jobs):
-        with torch.cuda.stream(stream):
-            parts.append(eng.results())
     merged = MetricsReport.new(trace=trace)
     for rep in reports:
         merged.timesteps += rep.timesteps
@@ -113,7 +86,7 @@ def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
         merged.simulated_cost += rep.simulated_cost
         if trace and rep.per_step_trace:
             merged.per_step_trace.extend(rep.per_step_trace)
-    return ConcurrentResults(len(corpus), shards, parts), merged
+    return out, merged
 
 
 def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast, streams=1):

@@ -105,7 +105,10 @@ class HostScorerAdapter:
     """Runs a reference-protocol Scorer (bb/model.py:78-87) inside the device
     engine: candidates of the step's rows are rebuilt on the host, score_next
     is called per row in beam order (bb/search.py:223-225) and the rows are
-    uploaded as normalised log-probs (fp32; K1 takes lse = 0)."""
+    uploaded as the scorer's own fp64 log-probs (bb/model.py:216-217): the
+    device selects the top-M by exact fp64 row value and adds those values in
+    fp64 (vs_row_topm_f64), so a reference scorer's decode is bit-identical to
+    the reference's — tokens, scores, events."""
 
     def __init__(self, scorer, corpus=None):
         self.inner = scorer
@@ -116,7 +119,7 @@ class HostScorerAdapter:
 
     def bind(self, engine) -> None:
         self.enc = {}
-        self._buf = torch.empty((engine.capacity, self.vocab.size), dtype=torch.float32,
+        self._buf = torch.empty((engine.capacity, self.vocab.size), dtype=torch.float64,
                                 device=engine.device)
 
     def on_admit(self, engine, status) -> None:
@@ -131,7 +134,7 @@ class HostScorerAdapter:
         if R is None:
             raise RuntimeError("HostScorerAdapter needs the host row count (synchronous driver)")
         if R == 0:
-            return self._buf, N.VS_DTYPE_F32 | N.VS_ROWS_NORMALIZED
+            return self._buf, N.VS_DTYPE_F64 | N.VS_ROWS_NORMALIZED
         t = engine.t
         slots = t["row_slot"][:R].cpu().numpy()
         cands = t["row_cand"][:R].cpu().numpy()
@@ -140,7 +143,7 @@ class HostScorerAdapter:
         k, L = engine.k, engine.max_len
         hist = t["hist"].view(-1, L)[torch.from_numpy(phys).to(engine.device).long()].cpu().numpy()
         score = t["c_score"][(torch.from_numpy(slots * k + cands)).to(engine.device).long()].cpu().numpy()
-        rows = np.empty((R, self.vocab.size), dtype=np.float32)
+        rows = np.empty((R, self.vocab.size), dtype=np.float64)
         for r in range(R):
             enc = self.enc[int(slots[r])]
             cand = Candidate(tuple(int(x) for x in hist[r, :lens[r]]), float(score[r]), False,
@@ -151,7 +154,7 @@ class HostScorerAdapter:
                                 f"{self.vocab.size}")
             rows[r] = np.asarray(row, dtype=np.float64)
         self._buf[:R].copy_(torch.from_numpy(rows))
-        return self._buf, N.VS_DTYPE_F32 | N.VS_ROWS_NORMALIZED
+        return self._buf, N.VS_DTYPE_F64 | N.VS_ROWS_NORMALIZED
 
     def after_step(self, engine, R) -> None:
         pass

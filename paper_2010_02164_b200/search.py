@@ -95,80 +95,126 @@ def proj_lse_topm(h: torch.Tensor, w: torch.Tensor, M: int, *, eos: int = -1, eo
     return tok, lp, lse, fb, lg[:, :V]
 
 
-def _load_beam(eng: SearchEngine, beam: Beam) -> int:
-    """Write one beam into slot 0 of a 1-slot engine; returns its active width."""
-    k, L = eng.k, eng.max_len
-    w = len(beam.candidates)
-    t = eng.t
-    t["slot_input"][0] = 0
-    t["slot_lt"][0] = beam.l_t
-    t["slot_emitted"][0] = beam.emitted
-    t["slot_width"][0] = w
-    nact = beam.active_width()
-    t["slot_active"][0] = nact
-    t["slot_flags"][0] = 1
-    hist = np.zeros((k, L), dtype=np.int32)
-    for j, c in enumerate(beam.candidates):
-        hist[j, : len(c.tokens)] = c.tokens
-    t["hist"].view(k, L).copy_(torch.from_numpy(hist))
-    t["c_score"][:w] = torch.tensor([c.score for c in beam.candidates], dtype=torch.float64)
-    t["c_len"][:w] = torch.tensor([len(c.tokens) for c in beam.candidates], dtype=torch.int32)
-    t["c_row"][:w] = torch.arange(w, dtype=torch.int32)
-    t["c_fin"][:w] = torch.tensor([int(c.finalized) for c in beam.candidates], dtype=torch.uint8)
-    st = np.zeros(N.status_ints(1), dtype=np.int32)
-    st[N.ST_R], st[N.ST_NSEL] = nact, 1
+_EXPAND_ENGINES: dict = {}
+
+
+def _expand_engine(config: DecodeConfig, vocab: Vocabulary, n_beams: int, drain: bool) -> SearchEngine:
+    """A cached engine with >= n_beams slots for per-beam expansion calls."""
+    n = 1 << max(0, (n_beams - 1).bit_length())
+    key = (config.k, config.max_candidates, config.delta, config.max_len, str(config.policy),
+           vocab.size, vocab.sos, vocab.eos, n, torch.cuda.current_device())
+    eng = _EXPAND_ENGINES.pop(key, None)
+    if eng is None:
+        while len(_EXPAND_ENGINES) >= 16:  # a small LRU: per-beam callers reuse a few shapes
+            _EXPAND_ENGINES.pop(next(iter(_EXPAND_ENGINES)))
+        cfg = DecodeConfig(k=config.k, n=n, epsilon=config.epsilon, delta=config.delta,
+                           max_candidates=config.max_candidates, max_len=config.max_len, policy=config.policy)
+        eng = SearchEngine(cfg, vocab)
+    _EXPAND_ENGINES[key] = eng
+    eng.cfg.no_drain = 0 if drain else 1
+    return eng
+
+
+def _load_beams(eng: SearchEngine, beams) -> list[int]:
+    """Write beam b into slot b (slot_input = b, its emissions go to output
+    row b); returns the active widths.  One H2D per field."""
+    k, L, B = eng.k, eng.max_len, len(beams)
+    eng.load_corpus([[0]] * B)
+    widths = [len(b.candidates) for b in beams]
+    nact = [b.active_width() for b in beams]
+    hist = np.zeros((B, k, L), dtype=np.int32)
+    score = np.zeros((B, k), dtype=np.float64)
+    clen = np.zeros((B, k), dtype=np.int32)
+    fin = np.zeros((B, k), dtype=np.uint8)
+    for b, beam in enumerate(beams):
+        for j, c in enumerate(beam.candidates):
+            hist[b, j, : len(c.tokens)] = c.tokens
+            score[b, j], clen[b, j], fin[b, j] = c.score, len(c.tokens), int(c.finalized)
+    t, dev = eng.t, eng.device
+    i32 = lambda x: torch.tensor(x, dtype=torch.int32)  # noqa: E731
+    t["slot_input"][:B] = i32(list(range(B))).to(dev)
+    t["slot_lt"][:B] = i32([b.l_t for b in beams]).to(dev)
+    t["slot_emitted"][:B] = i32([b.emitted for b in beams]).to(dev)
+    t["slot_width"][:B] = i32(widths).to(dev)
+    t["slot_active"][:B] = i32(nact).to(dev)
+    t["slot_flags"][:B] = 1
+    t["hist"].view(-1, k, L)[:B].copy_(torch.from_numpy(hist))
+    t["c_score"].view(-1, k)[:B].copy_(torch.from_numpy(score))
+    t["c_len"].view(-1, k)[:B].copy_(torch.from_numpy(clen))
+    t["c_row"].view(-1, k)[:B] = torch.arange(k, dtype=torch.int32, device=dev)
+    t["c_fin"].view(-1, k)[:B].copy_(torch.from_numpy(fin))
+    st = np.zeros(N.status_ints(eng.n), dtype=np.int32)
+    st[N.ST_R], st[N.ST_NSEL] = sum(nact), B
     t["status"].copy_(torch.from_numpy(st))
-    t["sel"][0] = 0
-    t["sel_off"][:2] = torch.tensor([0, nact], dtype=torch.int32)
+    t["sel"][:B] = i32(list(range(B))).to(dev)
+    t["sel_off"][: B + 1] = i32(np.concatenate([[0], np.cumsum(nact)]).tolist()).to(dev)
     t["n_copy"].zero_()
+    t["counters"].zero_()
+    t["out_len"].zero_()  # emission slots below beam.emitted are never written
+    t["out_off"].zero_()
     return nact
 
 
-def expand_beam(beam: Beam, score_rows, config: DecodeConfig, vocab: Vocabulary,
-                *, drain: bool = False):
-    """Device expand_beam (bb/search.py:76-103).  Rows are per-active-candidate
-    log-prob vectors in beam order; they are rounded to fp32 on upload (the
-    kernel contract: logp = fp32(row)).  drain=True adds advance_beam's
-    length-cap drain (bb/search.py:227-229)."""
-    if not beam.candidates:
-        raise InvariantViolation("cannot expand an empty beam")
-    nact = beam.active_width()
-    if str(getattr(config.policy, "value", config.policy)) == "immediate" and nact != len(beam.candidates):
-        raise InvariantViolation("immediate policy never keeps finalized candidates on the beam")
-    if len(score_rows) != nact:
-        raise InvariantViolation(f"expected {nact} score rows, got {len(score_rows)}")
-    for row in score_rows:
-        if len(row) != vocab.size:
-            raise InvariantViolation(
-                f"score row of length {len(row)} for vocabulary of size {vocab.size}")
-    cfg1 = DecodeConfig(k=config.k, n=1, epsilon=config.epsilon, delta=config.delta,
-                        max_candidates=config.max_candidates, max_len=config.max_len,
-                        policy=config.policy)
-    eng = SearchEngine(cfg1, vocab)
-    eng.cfg.no_drain = 0 if drain else 1
-    eng.load_corpus([[vocab.sos]])
-    _load_beam(eng, beam)
-    rows = torch.tensor(np.asarray(score_rows, dtype=np.float64).reshape(nact, vocab.size),
-                        dtype=torch.float32).to(eng.device)
-    if nact:
-        eng.row_topm(rows, N.VS_DTYPE_F32 | N.VS_ROWS_NORMALIZED, nact, nact)
+def expand_beams(beams, score_rows, config: DecodeConfig, vocab: Vocabulary, *, drain: bool = False):
+    """bb/search.py:76-103 (expand_beam) for several beams in ONE device step:
+    K1-f64 over all their rows, then one beam-step launch (one CTA per beam).
+    ``score_rows[b]`` are beam b's per-active-candidate log-prob rows in beam
+    order, kept in fp64 end to end (top-M by exact row value, fp64 score
+    adds), so each result is the reference's bit for bit.  drain=True adds
+    advance_beam's length-cap drain (bb/search.py:227-229).  Returns
+    [(next beam, emitted candidates)] in input order."""
+    policy_imm = str(getattr(config.policy, "value", config.policy)) == "immediate"
+    for beam, rows in zip(beams, score_rows):
+        if not beam.candidates:
+            raise InvariantViolation("cannot expand an empty beam")
+        nact = beam.active_width()
+        if policy_imm and nact != len(beam.candidates):
+            raise InvariantViolation("immediate policy never keeps finalized candidates on the beam")
+        if len(rows) != nact:
+            raise InvariantViolation(f"expected {nact} score rows, got {len(rows)}")
+        for row in rows:
+            if len(row) != vocab.size:
+                raise InvariantViolation(
+                    f"score row of length {len(row)} for vocabulary of size {vocab.size}")
+    if not beams:
+        return []
+    if len(beams) > N.VS_MAX_SLOTS:
+        return [r for b0 in range(0, len(beams), N.VS_MAX_SLOTS)
+                for r in expand_beams(beams[b0:b0 + N.VS_MAX_SLOTS], score_rows[b0:b0 + N.VS_MAX_SLOTS],
+                                      config, vocab, drain=drain)]
+    eng = _expand_engine(config, vocab, len(beams), drain)
+    nact = _load_beams(eng, beams)
+    R = sum(nact)
+    if R:  # the rows' own fp64 values (bb/search.py:69-71): vs_row_topm_f64
+        flat = np.asarray([r for rows in score_rows for r in rows], dtype=np.float64).reshape(R, vocab.size)
+        eng.row_topm(torch.from_numpy(flat).to(eng.device), N.VS_DTYPE_F64 | N.VS_ROWS_NORMALIZED, R, R)
     eng.beam_step()
     t = eng.t
     if int(t["counters"][3]):  # device-detected contract break (bb/search.py:155-158 etc.)
         raise InvariantViolation(f"beam step error {int(t['counters'][3])}")
-    k, L = eng.k, eng.max_len
-    width = int(t["slot_width"][0])
-    emitted_total = int(t["slot_emitted"][0])
-    sc = t["c_score"][:width].cpu().numpy()
-    ln = t["c_len"][:width].cpu().numpy()
-    rw = t["c_row"][:width].cpu().numpy()
-    fz = t["c_fin"][:width].cpu().numpy()
-    hist = t["hist"].view(k, L).cpu().numpy()
-    nxt = tuple(Candidate(tuple(int(x) for x in hist[rw[j], : ln[j]]), float(sc[j]), bool(fz[j]),
-                          beam.input_id) for j in range(width))
+    k, L, B = eng.k, eng.max_len, len(beams)
+    width = t["slot_width"][:B].cpu().tolist()
+    emitted_total = t["slot_emitted"][:B].cpu().tolist()
+    sc = t["c_score"].view(-1, k)[:B].cpu().numpy()
+    ln = t["c_len"].view(-1, k)[:B].cpu().numpy()
+    rw = t["c_row"].view(-1, k)[:B].cpu().numpy()
+    fz = t["c_fin"].view(-1, k)[:B].cpu().numpy()
+    hist = t["hist"].view(-1, k, L)[:B].cpu().numpy()
     res = eng.results()
-    emitted = [Candidate(c.tokens, c.score, True, beam.input_id)
-               for c in res[0][beam.emitted:emitted_total]]
-    # results() marks emitted candidates finalized; a length-cap straggler is
-    # emitted with finalized=True by the reference too (bb/search.py:194).
-    return Beam(beam.input_id, nxt, beam.l_t + 1, emitted_total), emitted
+    out = []
+    for b, beam in enumerate(beams):
+        nxt = tuple(Candidate(tuple(int(x) for x in hist[b, rw[b, j], : ln[b, j]]), float(sc[b, j]),
+                              bool(fz[b, j]), beam.input_id) for j in range(width[b]))
+        # emitted candidates are finalized; a length-cap straggler is emitted
+        # with finalized=True by the reference too (bb/search.py:194)
+        emitted = [Candidate(c.tokens, c.score, True, beam.input_id)
+                   for c in res[b][beam.emitted:emitted_total[b]]]
+        out.append((Beam(beam.input_id, nxt, beam.l_t + 1, emitted_total[b]), emitted))
+    return out
+
+
+def expand_beam(beam: Beam, score_rows, config: DecodeConfig, vocab: Vocabulary,
+                *, drain: bool = False):
+    """Device expand_beam (bb/search.py:76-103): ``expand_beams`` for one beam.
+    Returns (next beam, emitted list)."""
+    return expand_beams([beam], [score_rows], config, vocab, drain=drain)[0]

@@ -1,0 +1,80 @@
+"""CPU checks of the host-side API pieces (paper_2010_02164_b200.api) against
+the oracle restatement of bb/heuristics.py and bb/scheduler.py."""
+import math
+import random
+
+import pytest
+
+from oracle import varstream_oracle as O
+from paper_2010_02164_b200 import api as A
+from paper_2010_02164_b200.core import Beam, Candidate, DecodeConfig, Proposal, Vocabulary
+from paper_2010_02164_b200.errors import ConfigError, InvariantViolation
+
+
+def _pool(rng, n):
+    pool = []
+    for _ in range(n):
+        tok = None if rng.random() < 0.15 else rng.randrange(20)
+        pool.append(Proposal(round(-rng.random() * 4, rng.choice([1, 2, 6])), rng.randrange(6), tok))
+    return pool
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_apply_heuristics_matches_oracle(seed):
+    rng = random.Random(seed)
+    pool = _pool(rng, rng.randrange(1, 40))
+    k, M = rng.randrange(1, 9), rng.randrange(1, 5)
+    delta = rng.choice([0.0, 0.5, 1.5, math.inf])
+    got = A.apply_heuristics(pool, k=k, delta=delta, max_candidates=M)
+    opool = [O.Proposal(p.score, p.parent, p.token) for p in pool]
+    want = O.apply_heuristics(opool, k=k, delta=delta, max_candidates=M)
+    assert [tuple(p) for p in got] == [tuple(p) for p in want]
+    assert A.HeuristicConfig(delta, M).apply(pool, k) == got
+
+
+def test_heuristic_config_and_empty_pool_errors():
+    with pytest.raises(ConfigError):
+        A.HeuristicConfig(-1.0, 2)
+    with pytest.raises(ConfigError):
+        A.HeuristicConfig(1.0, 0)
+    with pytest.raises(InvariantViolation):
+        A.apply_heuristics([], k=2, delta=1.0, max_candidates=1)
+
+
+class _Enc:
+    def __init__(self, i):
+        self.input_id = i
+
+
+class _Sc:
+    vocab = Vocabulary(10, 0, 1)
+
+    def encode(self, toks, input_id=0):
+        return _Enc(input_id)
+
+
+def test_refill_and_selection_match_oracle():
+    cfg = DecodeConfig(k=3, n=5, capacity=7)
+    st = A.BatchState()
+    ost = O.BatchState()
+
+    class OSc:
+        sos = 0
+
+        def encode(self, toks, input_id=0):
+            return _Enc(input_id)
+
+    corpus = [(1, 2)] * 9
+    assert A.refill(st, corpus, cfg, _Sc()) == O.refill(ost, corpus, O.as_oconfig(cfg), OSc()) == [0, 1, 2, 3, 4]
+    widths = [(2, 3), (3, 1), (2, 2), (1, 4), (3, 2)]  # (l_t, active width)
+    for s, os_, (lt, w) in zip(st.beams, ost.beams, widths):
+        cands = tuple(Candidate((0,) * lt, -0.1 * j, False, s.input_id) for j in range(w))
+        s.beam = Beam(s.input_id, cands, lt, 0)
+        os_.beam = O.Beam(s.input_id, tuple(O.Candidate(c.tokens, c.score, False, s.input_id) for c in cands), lt, 0)
+    for mine, ref in ((A.select_min_lt, O.select_min_lt), (A.select_fifo_max_lt, O.select_fifo_max_lt)):
+        sel = mine(st, cfg.capacity)
+        chosen, total, eff = ref(ost, cfg.capacity)
+        assert [s.input_id for s in sel.selected] == [s.input_id for s in chosen]
+        assert (sel.total_expansions, sel.effective_len) == (total, eff)
+    with pytest.raises(ConfigError):
+        A.select_min_lt(st, 2)

@@ -4,7 +4,7 @@ import json
 import pytest
 
 from paper_2010_02164_b200 import cli
-from paper_2010_02164_b200.harness import (ResultsDocument, generate_synthetic_corpus, load_corpus,
+from paper_2010_02164_b200.harness import (Corpus, ResultsDocument, generate_synthetic_corpus, load_corpus,
                                            save_corpus)
 from paper_2010_02164_b200.errors import DataError
 
@@ -13,7 +13,8 @@ def test_corpus_round_trip_and_errors(tmp_path):
     c = [(1, 2, 3), (4,), (5, 6)]
     p = tmp_path / "c.txt"
     save_corpus(c, p)
-    assert load_corpus(p) == c
+    got = load_corpus(p)
+    assert isinstance(got, Corpus) and got.inputs == tuple(c) and len(got) == 3 and got[1] == (4,)
     (tmp_path / "bad.txt").write_text("1 2\nx 3\n")
     with pytest.raises(DataError, match="line 2"):
         load_corpus(tmp_path / "bad.txt")
@@ -76,3 +77,39 @@ def test_cli_device_run_writes_results_and_trace(tmp_path):
     doc = ResultsDocument.read(out)
     assert len(doc.records) == 40 and all(1 <= len(r["candidates"]) <= 5 for r in doc.records)
     assert (tmp_path / "r.json.trace.csv").read_text().startswith("timestep,expansions")
+
+
+def test_experiment_config_validation_matches_reference():
+    """bb/harness.py:140-168: engine name, exactly one corpus source, trace
+    needs an output path, fixed engines need pruning off."""
+    import math
+
+    from paper_2010_02164_b200.core import DecodeConfig
+    from paper_2010_02164_b200.errors import ConfigError
+    from paper_2010_02164_b200.harness import ExperimentConfig, SyntheticCorpusSpec
+
+    m = {"kind": "device_hash", "vocab_size": 50, "sos": 0, "eos": 1}
+    dec = DecodeConfig(k=3, n=4)
+    syn = SyntheticCorpusSpec.from_dict({"n_inputs": 5})
+    ExperimentConfig("varstream", m, dec, synthetic=syn)
+    for bad in (dict(engine="nope", synthetic=syn), dict(engine="varstream"),
+                dict(engine="varstream", synthetic=syn, corpus_path="x"),
+                dict(engine="varstream", synthetic=syn, trace=True),
+                dict(engine="fixed", synthetic=syn, decode=DecodeConfig(k=3, n=4, delta=1.5))):
+        eng, d = bad.pop("engine"), bad.pop("decode", dec)
+        with pytest.raises(ConfigError):
+            ExperimentConfig(eng, m, d, **bad)
+    ExperimentConfig("fixed", m, DecodeConfig(k=3, n=4, delta=math.inf, max_candidates=3), synthetic=syn)
+    with pytest.raises(ConfigError):
+        SyntheticCorpusSpec.from_dict({"mean_len": 3})
+
+
+def test_cli_rejects_out_of_scope_model_kinds(tmp_path):
+    """The reference's seeded-hash / n-gram scorers are out of scope and the
+    CLI never imports the reference package: exit code 2 with a message."""
+    mp = tmp_path / "m.json"
+    mp.write_text(json.dumps({"kind": "seeded_hash", "vocab_size": 50, "sos": 0, "eos": 1, "seed": 3}))
+    cp = tmp_path / "c.txt"
+    cp.write_text("3 4 5\n")
+    assert cli.main(["--engine", "varstream", "--k", "2", "--n", "2", "--model", str(mp),
+                     "--corpus", str(cp)]) == 2

@@ -102,20 +102,23 @@ def test_row_topm_tma_split_rows(R, dtype, M):
     _check_rows(x[pick], M, tok.cpu().numpy()[pick], lp.cpu().numpy()[pick], lse.cpu().numpy()[pick])
 
 
+@pytest.mark.parametrize("kernel", ["split", "warp"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_row_topm_tma_lse_is_partition_invariant(dtype):
+def test_row_topm_lse_is_partition_invariant(dtype, kernel):
     """lse (hence every logp) of a row is a function of the row alone: the same
-    row scored alone, among 5 rows, or among 900 rows (different split of its
-    segments over warps) gives bit-identical outputs."""
+    row scored alone, among 5 rows, among 900 or among 6,400 rows (different
+    splits of its segments over warps: the warp kernel picks 8, 4, 2 or 1 warps
+    per row from the live row count) gives bit-identical outputs — so an
+    input's decode does not depend on what else shares its batch."""
     P, *_ = _pkg()
-    rng = np.random.default_rng(11)
-    V, M = 42024, 8
-    base = rng.normal(0, 2, (900, V)).astype(np.float32)
+    V, M = 42024, 5
+    g = torch.Generator(device="cuda").manual_seed(11)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
-    big = torch.from_numpy(base).cuda().to(tdt)
+    big = (torch.randn((6400, V), generator=g, device="cuda") * 2.0).to(tdt)
+    big[450, 7] = 40.0  # a late max raise inside one segment
     outs = []
-    for lo, hi in [(450, 451), (448, 453), (0, 900), (300, 901)]:
-        tok, lp, lse, _ = P.row_lse_topm(big[lo:hi].contiguous(), M, kernel="split")
+    for lo, hi in [(450, 451), (448, 453), (0, 900), (300, 1000), (0, 6400)]:
+        tok, lp, lse, _ = P.row_lse_topm(big[lo:hi], M, kernel=kernel)
         outs.append((tok[450 - lo].cpu(), lp[450 - lo].cpu(), lse[450 - lo].cpu()))
     for o in outs[1:]:
         assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) and torch.equal(o[2], outs[0][2])
@@ -161,53 +164,63 @@ def _ocfg(d):
                      max_candidates=d["max_candidates"], max_len=d["max_len"], policy=d["policy"])
 
 
+def _golden_beam(P, case):
+    cands = tuple(P.Candidate(tuple(c["tokens"]), fl(c["score"]), c["finalized"])
+                  for c in case["beam"]["candidates"])
+    return P.Beam(0, cands, case["beam"]["l_t"], case["beam"]["emitted"])
+
+
+def _check_golden_expand(case, got, emitted, ci):
+    w = case["want"]
+    key = lambda c: (tuple(c.tokens), c.score, bool(c.finalized))  # noqa: E731
+    assert [key(c) for c in got.candidates] == [
+        (tuple(c["tokens"]), fl(c["score"]), c["finalized"]) for c in w["next"]], ci
+    assert [(c.tokens, c.score) for c in emitted] == [(tuple(c["tokens"]), fl(c["score"])) for c in w["emitted"]], ci
+    assert got.emitted == w["emitted_total"] and got.l_t == w["l_t"], ci
+
+
 def test_device_expand_beam_matches_reference_goldens():
-    """Every golden case of the reference's expand_beam — deferred (incl. the
-    row-value pre-truncation gap case) and immediate — through K1+K2."""
+    """Every golden case of the REFERENCE's expand_beam (deferred, incl. the
+    row-value pre-truncation gap case, and immediate) through K1-f64 + K2:
+    next beam, emissions and every fp64 score bit-identical to the reference's
+    own recorded outputs (the rows stay fp64)."""
     P, *_ = _pkg()
     for ci, case in enumerate(EXPAND):
-        d = case["config"]
+        d, v = case["config"], case["vocab"]
         cfg = P.DecodeConfig(k=d["k"], n=1, delta=fl(d["delta"]), max_candidates=d["max_candidates"],
                              max_len=d["max_len"], policy=d["policy"])
-        v = case["vocab"]
         vocab = P.Vocabulary(v["size"], v["sos"], v["eos"])
-        cands = tuple(P.Candidate(tuple(c["tokens"]), fl(c["score"]), c["finalized"])
-                      for c in case["beam"]["candidates"])
-        beam = P.Beam(0, cands, case["beam"]["l_t"], case["beam"]["emitted"])
         rows = [[fl(x) for x in r] for r in case["rows"]]
-        got, emitted = P.expand_beam(beam, rows, cfg, vocab)
-        # oracle on the fp32-rounded rows the kernel contract sees
-        r32 = [np.asarray(r, dtype=np.float32).astype(np.float64) for r in rows]
-        ob = O.Beam(0, tuple(O.Candidate(c.tokens, c.score, c.finalized) for c in cands),
-                    beam.l_t, beam.emitted)
-        want, wem = O.expand_beam(ob, r32, _ocfg(d), v["size"], v["eos"])
-        key = lambda c: (tuple(c.tokens), c.score, bool(c.finalized))  # noqa: E731
-        assert [key(c) for c in got.candidates] == [key(c) for c in want.candidates], ci
-        assert [(c.tokens, c.score) for c in emitted] == [(c.tokens, c.score) for c in wem], ci
-        assert got.emitted == want.emitted
-        if all(float(np.float32(x)) == x for r in rows for x in r):  # fp32-exact rows
-            assert [key(c) for c in got.candidates] == [
-                (tuple(c["tokens"]), fl(c["score"]), c["finalized"]) for c in case["want"]["next"]]
+        got, emitted = P.expand_beam(_golden_beam(P, case), rows, cfg, vocab)
+        _check_golden_expand(case, got, emitted, ci)
+
+
+def test_expand_beams_batches_many_beams_in_one_step():
+    """expand_beams: the golden cases that share a configuration, expanded
+    together (one K1-f64 + one beam-step launch), each equal to the reference."""
+    import json
+
+    P, *_ = _pkg()
+    groups = {}
+    for ci, case in enumerate(EXPAND):
+        groups.setdefault(json.dumps([case["config"], case["vocab"]], sort_keys=True), []).append(ci)
+    big = sorted(groups.values(), key=len)[-6:]
+    assert max(len(g) for g in big) >= 3
+    for g in big:
+        case0 = EXPAND[g[0]]
+        d, v = case0["config"], case0["vocab"]
+        cfg = P.DecodeConfig(k=d["k"], n=1, delta=fl(d["delta"]), max_candidates=d["max_candidates"],
+                             max_len=d["max_len"], policy=d["policy"])
+        vocab = P.Vocabulary(v["size"], v["sos"], v["eos"])
+        beams = [_golden_beam(P, EXPAND[ci]) for ci in g]
+        rows = [[[fl(x) for x in r] for r in EXPAND[ci]["rows"]] for ci in g]
+        for ci, (got, emitted) in zip(g, P.expand_beams(beams, rows, cfg, vocab)):
+            _check_golden_expand(EXPAND[ci], got, emitted, ci)
 
 
 def _events(evs):
     return [(e.timestep, e.phase, tuple(e.refilled), tuple(e.selected), e.expansions,
              e.effective_len, tuple(e.finished), tuple(e.live_after)) for e in evs]
-
-
-class _F32Rows:
-    """Oracle-side view of a reference scorer with rows rounded to fp32 (the
-    device adapter uploads fp32 rows)."""
-
-    def __init__(self, inner):
-        self.inner = inner
-        self.vocab_size, self.sos, self.eos = inner.vocab_size, inner.sos, inner.eos
-
-    def encode(self, tokens, input_id=0):
-        return self.inner.encode(tokens, input_id)
-
-    def score_next(self, enc, cand):
-        return np.asarray(self.inner.score_next(enc, cand), dtype=np.float32).astype(np.float64)
 
 
 class _RefVocabScorer:
@@ -226,13 +239,19 @@ class _RefVocabScorer:
 RUNS = {f["name"]: f for f in load("runs.json")}
 
 
-@pytest.mark.parametrize("name", ["c1_varstream_eps0.1667", "c1_varbeam", "c1_varfifo",
-                                  "c1_varstream_flush7", "c1_varstream_cap23", "c1_fixedstream",
-                                  "c1_varstream_immediate"])
-def test_engine_with_reference_scorer_matches_oracle_events(name):
-    """Reference workloads (SeededHashScorer) through the device engine via the
-    drop-in adapter: StepEvents, trace and outputs bit-exact vs the oracle
-    given the same (fp32) rows."""
+def _golden_events(evs):
+    return [(e["timestep"], e["phase"], tuple(e["refilled"]), tuple(e["selected"]), e["expansions"],
+             e["effective_len"], tuple(e["finished"]), tuple(e["live_after"])) for e in evs]
+
+
+@pytest.mark.parametrize("name", sorted(RUNS))
+def test_engine_with_reference_scorer_matches_reference_runs(name):
+    """The unmodified reference workloads (SeededHashScorer, fp64 log-prob rows)
+    driven through the device engine via the drop-in adapter reproduce the
+    REFERENCE's own recorded run (tests/golden/runs.json, written by
+    oracle/gen_golden.py from bb/scheduler.py): every StepEvent, the per-step
+    trace, the simulated cost, and every output token and fp64 score
+    bit-exactly (the rows stay fp64 end to end: vs_row_topm_f64)."""
     P, N, SearchEngine, _, HostScorerAdapter, _ = _pkg()
     fx = RUNS[name]
     s = fx["scorer"]
@@ -242,20 +261,47 @@ def test_engine_with_reference_scorer_matches_oracle_events(name):
                          max_candidates=d["max_candidates"], max_len=d["max_len"],
                          capacity=d["capacity"], flush_interval=d["flush_interval"],
                          policy=d["policy"])
-    corpus = [tuple(x) for x in fx["corpus"]][:120]
+    corpus = [tuple(x) for x in fx["corpus"]]
     vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
     runner = {"run_varstream": P.run_varstream, "run_varbeam": P.run_varbeam,
               "run_varfifo": P.run_varfifo}[fx["runner"]]
     ev = []
     out, rep = runner(corpus, _RefVocabScorer(base, vocab), cfg, trace=True, on_step=ev.append)
-    oev = []
-    oref = {"run_varstream": O.run_varstream, "run_varbeam": O.run_varbeam,
-            "run_varfifo": O.run_varfifo}[fx["runner"]]
-    want, wrep = oref(corpus, _F32Rows(base), O.as_oconfig(cfg), trace=True, on_step=oev.append)
-    assert _events(ev) == _events(oev)
-    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
-    assert [tuple(r) for r in rep.per_step_trace] == [tuple(r) for r in wrep.per_step_trace]
-    assert rep.simulated_cost == wrep.simulated_cost
+    assert _events(ev) == _golden_events(fx["events"])
+    want = [[(tuple(c["tokens"]), fl(c["score"])) for c in per] for per in fx["outputs"]]
+    assert [[(c.tokens, c.score) for c in per] for per in out] == want
+    r = fx["report"]
+    assert rep.timesteps == r["timesteps"] and rep.candidate_expansions == r["candidate_expansions"]
+    assert [list(x) for x in rep.per_step_trace] == [list(x) for x in r["trace"]]
+    assert rep.simulated_cost == r["simulated_cost"]
+
+
+def test_row_topm_f64_matches_oracle():
+    """K1-f64 (vs_row_topm_f64): top-M of fp64 rows by (value desc, token asc),
+    exact values, ties, -inf, NaN never ranked, V < M padding."""
+    P, N, *_ = _pkg()
+    lib = N.load_library()
+    rng = np.random.default_rng(5)
+    for R, V, M in ((1, 1, 3), (7, 50, 5), (33, 1000, 12), (5, 4096, 64), (3, 300, 128)):
+        x = rng.standard_normal((R, V))
+        x[:, ::7] = np.round(x[:, ::7], 1)  # ties
+        if V > 4:
+            x[0, 1] = -np.inf
+            x[-1, 2] = np.nan
+        dx = torch.from_numpy(x).cuda()
+        tok = torch.empty(R * M, dtype=torch.int32, device="cuda")
+        lp = torch.empty(R * M, dtype=torch.float32, device="cuda")
+        lp64 = torch.empty(R * M, dtype=torch.float64, device="cuda")
+        rc = lib.vs_row_topm_f64(dx.data_ptr(), V, V, M, R, None, R, tok.data_ptr(), lp.data_ptr(),
+                                 lp64.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        tok, lp64 = tok.view(R, M).cpu().numpy(), lp64.view(R, M).cpu().numpy()
+        for r in range(R):
+            order = sorted((t for t in range(V) if x[r, t] == x[r, t]), key=lambda t: (-x[r, t], t))[:M]
+            assert list(tok[r, :len(order)]) == order
+            assert np.array_equal(lp64[r, :len(order)], x[r, order])
+            assert all(tok[r, len(order):] == -1)
 
 
 def test_greedy_engine_matches_reference_greedy_decode():
@@ -271,7 +317,7 @@ def test_greedy_engine_matches_reference_greedy_decode():
     corpus = [tuple(x) for x in fx["corpus"]][:80]
     vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
     out, rep = P.dispatch_engine("greedy", corpus, _RefVocabScorer(base, vocab), cfg, trace=True)
-    ref = _F32Rows(base)
+    ref = base
     want = [O.greedy_decode(ref.encode(x, i), ref, cfg.max_len) for i, x in enumerate(corpus)]
     assert [[(c.tokens, c.score) for c in per] for per in out] == [[(c.tokens, c.score)] for c in want]
     steps = sum(len(c.tokens) - 1 for c in want)
@@ -325,6 +371,48 @@ def test_device_hash_decode_matches_oracle(case):
         trace=True)
     assert [[(c.tokens, c.score) for c in per] for per in fast_out] == O.signature(want)
     assert fast_rep.per_step_trace == rep.per_step_trace
+
+
+# The bench's own workloads (bench.py WORKLOADS) at their exact engine shapes:
+# name, V, k, n, M, delta, max_len, N (a prefix of the bench's corpus
+# generator: geometric, seed 99), mean_len, clip, scorer seed, scale, eos_bias
+BENCH_SHAPES = [
+    ("wmt19_k50", 42024, 50, 128, 5, 1.5, 256, 320, 25.0, 200, 7, 0.5, 7.5),
+    ("parse_c3", 2048, 10, 256, 3, 10.0, 64, 1200, 12.0, None, 5, 0.5, 5.5),
+]
+
+
+@pytest.mark.parametrize("shape", BENCH_SHAPES, ids=[b[0] for b in BENCH_SHAPES])
+def test_bench_shape_decode_bit_exact_vs_oracle(shape):
+    """SURVEY §8(a) at the bench's exact engine shapes (C4: |V|=42,024, k=50,
+    n=128, M=5, δ=1.5; C3: |V|=2,048, k=10, n=256, M=3, δ=10), with enough
+    inputs that the ε-refill runs many times: every StepEvent, output token and
+    fp64 score bit-exact vs the oracle replaying the kernel's lse; the sync-free
+    graphed driver and the bench's 4 concurrent batches give the same outputs."""
+    name, V, k, n, M, delta, ml, Nin, mean, clip, seed, scale, eb = shape
+    P, N, SearchEngine, DeviceHashScorer, _, LseRecorder = _pkg()
+    vocab = P.Vocabulary(V, 0, 2)
+    cfg = P.DecodeConfig(k=k, n=n, epsilon=1 / 6, delta=delta, max_candidates=M, max_len=ml)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(99, Nin, V, mean_len=mean, clip=clip))
+    sc = DeviceHashScorer(vocab, seed, scale=scale, power=0, eos_bias=eb, dtype="bf16")
+    rec = LseRecorder(sc)
+    ev = []
+    out, rep = P.run_varstream(corpus, rec, cfg, trace=True, on_step=ev.append)
+    refills = sum(1 for e in ev if e.refilled)
+    assert refills >= 3, "the refill path was not exercised"
+    cpu = LseReplayScorer(HashLogitsCPU(V, 0, 2, seed, scale=scale, power=0, eos_bias=eb,
+                                        dtype="bf16"), rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    sig = O.signature(want)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == sig
+    assert rep.candidate_expansions == wrep.candidate_expansions
+    fast, frep = P.run_varstream(corpus, sc, cfg)
+    assert [[(c.tokens, c.score) for c in per] for per in fast] == sig
+    assert frep.candidate_expansions == wrep.candidate_expansions
+    many, _ = P.run_varstream(corpus, sc, cfg, streams=4)
+    assert [[(c.tokens, c.score) for c in per] for per in many] == sig
 
 
 def test_epsilon_and_scheduler_invariance_on_device():
@@ -672,3 +760,88 @@ def test_end_to_end_agreement_with_fp64_reference_rows():
         same += ok
     assert same / len(corpus) >= 0.995, (same, len(corpus))
     assert worst <= 1e-5
+
+
+def test_decoder_end_to_end_agreement_with_reference_search():
+    """north_star's decoder-path agreement: the device engine driving the
+    transformer decoder (fp32, physical-row K/V cache + K4, row kernels) vs
+    the REFERENCE search (oracle restatement of bb/scheduler.py run_varstream)
+    driving the same random-init model on the CPU through the stateless
+    Scorer protocol (oracle/scorers.py:TorchDecoderCPU, whole-prefix
+    recompute, fp64 log-softmax rows).  >= 99.5% of inputs identical (tokens
+    equal, scores within 1e-5 relative); every divergence is an fp near-tie:
+    the reference itself decided it by a margin <= 1e-4 (oracle/agreement.py)."""
+    from oracle.agreement import agreement_report
+    from oracle.scorers import TorchDecoderCPU
+    from paper_2010_02164_b200.decoder import TransformerScorer
+
+    P, *_ = _pkg()
+    V = 500
+    kw = dict(d=64, heads=4, layers=2, enc_layers=1, ffn=128, seed=3, tau=4.0)
+    vocab = P.Vocabulary(V, 0, 2)
+    cfg = P.DecodeConfig(k=5, n=16, epsilon=1 / 6, delta=2.5, max_candidates=3, max_len=24)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(21, 200, V, mean_len=6.0, clip=30))
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        dec = TransformerScorer(vocab, max_src=32, eos_bias=4.0, dtype=torch.float32, **kw)
+        out, rep = P.run_varstream(corpus, dec, cfg)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    cpu = TorchDecoderCPU(V, 0, 2, eos_bias=4.0, weights="f32", **kw)
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg))
+    ids = list(range(len(corpus)))
+    gsig = {i: [(c.tokens, c.score) for c in out[i]] for i in ids}
+    csig = dict(enumerate(O.signature(want)))
+    r = agreement_report(corpus, ids, gsig, csig, cpu, O.as_oconfig(cfg), tie_tol=1e-4)
+    assert r["identical_fraction"] >= 0.995, r
+    assert r["explained_by_near_ties"] == r["divergent"], r
+
+
+def test_api_per_beam_and_batch_pieces_reproduce_reference():
+    """The reference's own driver loop (bb/scheduler.py:243-287) written with
+    this package's API pieces — refill, select_min_lt, execute_step (all
+    selected beams expanded in one device step), flush_all — plus
+    beam_decode / greedy_decode per input, on the reference scorer: events,
+    outputs and fp64 scores equal the oracle's (pinned to the reference)."""
+    import math as _m
+
+    P, *_ = _pkg()
+    from paper_2010_02164_b200 import api as A
+
+    fx = RUNS["c1_varstream_flush7"]
+    s = fx["scorer"]
+    base = SeededHashScorerCPU(s["vocab_size"], s["sos"], s["eos"], s["seed"], s["eos_bias"])
+    vocab = P.Vocabulary(s["vocab_size"], s["sos"], s["eos"])
+    sc = _RefVocabScorer(base, vocab)
+    d = fx["config"]
+    cfg = P.DecodeConfig(k=d["k"], n=d["n"], epsilon=d["epsilon"], delta=fl(d["delta"]),
+                         max_candidates=d["max_candidates"], max_len=d["max_len"],
+                         flush_interval=d["flush_interval"])
+    corpus = [tuple(x) for x in fx["corpus"]][:70]
+    ev = []
+    state, rep = A.BatchState(), P.MetricsReport.new(trace=True)
+    thr = _m.floor(cfg.epsilon * cfg.n + 1e-9)
+    next_flush = cfg.flush_interval
+    while state.cursor < len(corpus) or state.beams:
+        if state.timestep >= next_flush:
+            if state.beams:
+                A.flush_all(state, sc, cfg, rep, ev.append)
+            next_flush = state.timestep + cfg.flush_interval
+        refilled = A.refill(state, corpus, cfg, sc) if len(state.beams) <= thr else []
+        if not state.beams:
+            break
+        A.execute_step(state, A.select_min_lt(state, cfg.capacity), sc, cfg, rep, refilled=refilled,
+                       on_step=ev.append)
+    out = [state.outputs[i] for i in range(len(corpus))]
+    oev = []
+    want, wrep = O.run_varstream(corpus, base, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    assert [tuple(r) for r in rep.per_step_trace] == [tuple(r) for r in wrep.per_step_trace]
+    for i in range(0, 70, 7):  # the unbatched reference per input, and greedy
+        enc = base.encode(corpus[i], i)
+        assert [(c.tokens, c.score) for c in A.beam_decode(enc, sc, cfg)] == O.signature([want[i]])[0]
+        g = A.greedy_decode(enc, sc, cfg.max_len)
+        og = O.greedy_decode(enc, base, cfg.max_len)
+        assert (g.tokens, g.score) == (og.tokens, og.score)

@@ -33,16 +33,22 @@ def _rank_main(rank, world, port, q):
     count = torch.zeros(n, dtype=torch.int32)
     lens = torch.full((n * K,), 99, dtype=torch.int32)  # garbage beyond count must be ignored
     scores = torch.full((n * K,), 7.0, dtype=torch.float64)
+    offs = torch.full((n * K,), 10 ** 6, dtype=torch.int32)
     toks = torch.full((n * K * L,), -5, dtype=torch.int32)
-    for li, g in enumerate(gids):
-        ex = _expected(int(g))
+    fill = 0
+    # the engine's append layout: emissions land in out_tok in device order,
+    # not input order (here: inputs in reverse)
+    for li in reversed(range(n)):
+        ex = _expected(int(gids[li]))
         count[li] = len(ex)
         for c, (t, sc) in enumerate(ex):
             o = li * K + c
             lens[o] = len(t)
             scores[o] = sc
-            toks[o * L:o * L + len(t)] = torch.tensor(t, dtype=torch.int32)
-    res = gather_results(pack_results(count, lens, scores, toks, K, L), N_TOTAL)
+            offs[o] = fill
+            toks[fill:fill + len(t)] = torch.tensor(t, dtype=torch.int32)
+            fill += len(t)
+    res = gather_results(pack_results(count, lens, scores, offs, toks, K), N_TOTAL)
     if rank == 0:
         got = [[(c.tokens, c.score) for c in res[g]] for g in range(N_TOTAL)]
         q.put(got)
