@@ -43,7 +43,7 @@ WORKLOADS = {
                    eos_bias=5.0, dtype="bf16"),
     # configs[2]: parsing shape
     "parse_c3": dict(V=2048, sos=0, eos=2, k=10, n=256, M=3, delta=10.0, eps=1 / 6, max_len=64,
-                     N=20000, mean_len=12.0, clip=None, seed=99, scorer_seed=5, scale=0.5, power=0,
+                     N=20000, mean_len=12.0, clip=128, seed=99, scorer_seed=5, scale=0.5, power=0,
                      eos_bias=5.5, dtype="bf16"),
 }
 METRIC = "decoded sequences/sec (ε-refill var-width beam, k=50); search-step HBM GB/s"
@@ -285,33 +285,24 @@ def engines_comparison(reps: int = 3):
     return out
 
 
-def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batches: int = 1):
-    """BASELINE.json configs[3] with its model: the same VarStream search
-    (k=50, n=128, M=5, δ=1.5, ε=1/6) scoring rows with a random-init
-    transformer-big decoder (6+6 layers, d=1024, FFN 4096, 16 heads,
-    |V|=42024, bf16; decoder.GraphedTransformerScorer).  Synchronous driver
-    (one status read per step), one CUDA-graph replay per decoder step.
-    Inputs: n_inputs taken evenly strided from the workload's length-sorted
-    corpus, so the length mix is the workload's."""
+def _model_leg(w, sample, make_scorer, batches: int, reps: int = 2, admit=None):
+    """Synchronous-driver decodes of `sample` with a model scorer: `batches`
+    concurrent refilling batches (weights shared, own caches; their drivers in
+    host threads on separate streams).  Returns (seconds, merged report, scorer)."""
+    import threading
+
     import torch
 
     from paper_2010_02164_b200 import DecodeConfig, Vocabulary
     from paper_2010_02164_b200 import _native as N
-    from paper_2010_02164_b200.decoder import GraphedTransformerScorer
     from paper_2010_02164_b200.engine import SearchEngine
+    from paper_2010_02164_b200.harness import shard
 
-    corpus = _corpus(w)
-    stride = max(1, len(corpus) // n_inputs)
-    sample = corpus[::stride][:n_inputs]
     vocab = Vocabulary(w["V"], w["sos"], w["eos"])
     cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
                        max_len=w["max_len"])
-    import threading
-
-    from paper_2010_02164_b200.harness import shard
-
-    dec = GraphedTransformerScorer(vocab, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0,
-                                   fused_head=fused_head)
+    admit = N.VS_ADMIT_VARSTREAM if admit is None else admit
+    dec = make_scorer(vocab)
     decs = [dec] + [dec.fork() for _ in range(batches - 1)]
     engs = [SearchEngine(cfg, vocab) for _ in range(batches)]
     subs = [[sample[int(i)] for i in shard(len(sample), batches, q)] for q in range(batches)]
@@ -320,14 +311,14 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batch
 
     def one(q):
         with torch.cuda.stream(streams[q]):
-            _, reps_out[q] = engs[q].run(subs[q], decs[q], admit_mode=N.VS_ADMIT_VARSTREAM,
+            _, reps_out[q] = engs[q].run(subs[q], decs[q], admit_mode=admit,
                                          select_mode=N.VS_SELECT_MIN_LT, flush_enabled=False)
 
     for q in range(batches):  # warm-up, one batch at a time: captures each batch's graphs
         one(q)
     torch.cuda.synchronize()
     times = []
-    for i in range(reps):  # the batches' synchronous drivers run in concurrent host threads
+    for i in range(reps):
         t0 = time.perf_counter()
         th = [threading.Thread(target=one, args=(q,)) for q in range(batches)]
         for x in th:
@@ -336,13 +327,31 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batch
             x.join()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
     rep = reps_out[0]
     for r_ in reps_out[1:]:
         rep.timesteps += r_.timesteps
         rep.candidate_expansions += r_.candidate_expansions
+    return statistics.median(times), rep, dec
+
+
+def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batches: int = 1):
+    """BASELINE.json configs[3] with its model: the same VarStream search
+    (k=50, n=128, M=5, δ=1.5, ε=1/6) scoring rows with a random-init
+    transformer-big decoder (6+6 layers, d=1024, FFN 4096, 16 heads,
+    |V|=42024, bf16; decoder.GraphedTransformerScorer).  Synchronous driver
+    (one status read per step), one CUDA-graph replay per decoder step.
+    Inputs: n_inputs taken evenly strided from the workload's length-sorted
+    corpus, so the length mix is the workload's."""
+    from paper_2010_02164_b200.decoder import GraphedTransformerScorer
+
+    corpus = _corpus(w)
+    stride = max(1, len(corpus) // n_inputs)
+    sample = corpus[::stride][:n_inputs]
+    t, rep, dec = _model_leg(w, sample, lambda v: GraphedTransformerScorer(
+        v, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0, fused_head=fused_head), batches, reps)
     return {"value": round(len(sample) / t, 2), "unit": "seq/s", "inputs": len(sample),
-            "sample": f"every {stride}th input of the {len(corpus)}-input length-sorted corpus",
+            "sample": "the whole corpus" if stride == 1 else
+                      f"every {stride}th input of the {len(corpus)}-input length-sorted corpus",
             "ms_per_decode": round(1e3 * t, 2), "timesteps": rep.timesteps,
             "ms_per_timestep": round(1e3 * t / rep.timesteps, 3),
             "expansions_per_step": round(rep.expansions_per_step, 1),
@@ -353,6 +362,60 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batch
             "head": "K5 tcgen05 projection + fused log-softmax/top-M" if fused_head
                     else "cuBLAS projection + K1",
             "graphs": len(dec.graphs)}
+
+
+LSTM_KW = dict(emb=128, hidden=256, max_src=128, seed=0, tau=4.0, eos_bias=3.0)
+
+
+def lstm_leg(reps: int = 2, batches: int = 2):
+    """BASELINE.json configs[2]: the lightweight LSTM parsing shape (|V|=2,048,
+    k=10, n=256, M=3, δ=10, N=20,000 synthetic) with its model — a 1-layer
+    LSTM encoder-decoder with attention (decoder.LSTMScorer), the latency-bound
+    small-step regime."""
+    from paper_2010_02164_b200.decoder import LSTMScorer
+
+    w = WORKLOADS["parse_c3"]
+    corpus = _corpus(w)
+    t, rep, dec = _model_leg(w, corpus, lambda v: LSTMScorer(v, **LSTM_KW), batches, reps)
+    return {"value": round(len(corpus) / t, 2), "unit": "seq/s", "inputs": len(corpus),
+            "ms_per_decode": round(1e3 * t, 2), "timesteps": rep.timesteps,
+            "us_per_timestep": round(1e6 * t / rep.timesteps, 1),
+            "expansions_per_step": round(rep.expansions_per_step, 1),
+            "workload": f"parse_c3: |V|={w['V']} k={w['k']} n={w['n']} M={w['M']} delta={w['delta']} eps=1/6 "
+                        f"max_len={w['max_len']} N={len(corpus)} (geometric mean {w['mean_len']}, clip {w['clip']})",
+            "model": "1-layer LSTM encoder-decoder, emb 128, hidden 256, 4x64-head dot attention, random init "
+                     "(seed 0), bf16 operands / fp32 cell", "concurrent_batches": batches,
+            "driver": "synchronous (status read per step), decoder step = 1 CUDA-graph replay per row bucket"}
+
+
+def toy_model_engines(reps: int = 2):
+    """BASELINE.json configs[0]/[1] with a small random-init decoder: Fixed vs
+    VarBeam vs FixedStream vs VarStream (ε sweep) on the toy workload
+    (|V|=1k, k=5, n=32, N=512), scoring with a 2+2-layer d=256 transformer
+    (decoder.GraphedTransformerScorer).  Outputs of the var-width engines are
+    identical (tested); only scheduling differs."""
+    import math
+
+    from paper_2010_02164_b200 import _native as N
+    from paper_2010_02164_b200.decoder import GraphedTransformerScorer
+
+    w = WORKLOADS["toy_c1"]
+    corpus = _corpus(w)
+    out = {}
+    runs = [("fixed", N.VS_ADMIT_VARBEAM, 1 / 6, math.inf, w["k"]),
+            ("varbeam", N.VS_ADMIT_VARBEAM, 1 / 6, w["delta"], w["M"]),
+            ("fixedstream", N.VS_ADMIT_VARSTREAM, 1 / 6, math.inf, w["k"])]
+    runs += [(f"varstream_eps1/{d}", N.VS_ADMIT_VARSTREAM, 1 / d, w["delta"], w["M"]) for d in (8, 6, 4)]
+    mk = lambda v: GraphedTransformerScorer(v, d=256, heads=4, layers=2, enc_layers=2, ffn=1024,  # noqa: E731
+                                            max_src=64, seed=0, tau=3.0, eos_bias=3.0)
+    for name, admit, eps, delta, M in runs:
+        wq = dict(w, eps=eps, delta=delta, M=M)
+        t, rep, _ = _model_leg(wq, corpus, mk, 1, reps, admit=admit)
+        out[name] = {"seq_per_s": round(len(corpus) / t, 1), "timesteps": rep.timesteps,
+                     "expansions": rep.candidate_expansions,
+                     "expansions_per_step": round(rep.expansions_per_step, 1)}
+    out["model"] = "transformer 2+2 layers d=256 ffn=1024 heads=4, random init (seed 0), bf16"
+    return out
 
 
 DEC_TAU, DEC_EOS_BIAS = 6.0, 20.0
@@ -631,6 +694,9 @@ def run_ours(args):
     }
     if rank == 0 and world == 1:
         line["engines_toy_c2"] = engines_comparison()
+        if args.model_legs:
+            line["engines_toy_c2_model"] = toy_model_engines()
+            line["lstm_parse_c3"] = lstm_leg()
     if rank == 0 and world == 1 and args.decoder_inputs > 0:
         line["decoder_wmt19"] = decoder_leg(w, args.decoder_inputs, batches=3)
         line["decoder_wmt19_k5"] = decoder_leg(w, args.decoder_inputs, fused_head=True, batches=3)
@@ -693,6 +759,8 @@ def main():
                     help="concurrent refilling batches (n slots each) per GPU, on separate CUDA streams")
     ap.add_argument("--decoder-cpu-baseline", action="store_true",
                     help="also time the reference search + CPU transformer scorer (8 inputs, ~3.5 min)")
+    ap.add_argument("--no-model-legs", dest="model_legs", action="store_false",
+                    help="skip the configs[0-2] model legs (toy transformer engines, C3 LSTM)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: N inputs per rank; strong: --strong-n inputs over all ranks (configs[4])")
     ap.add_argument("--strong-n", type=int, default=100000)

@@ -248,7 +248,9 @@ int vs_schedule_mirror(const vs_config* cfg, const vs_state* st, int32_t N, int3
  * stateless; bb/core.py:170 copies token tuples).  Applies copy_list: for
  * each (src, dst, len) copies positions [0,len) of `planes` planes, each
  * plane laid out as [rows, pos_stride_bytes*max_pos] with plane_stride_bytes
- * between planes.  Sources are never destinations (by construction in
+ * between planes.  pos_bytes < 0 selects fixed-size records: every copy
+ * moves exactly -pos_bytes bytes (per-row recurrent state such as an LSTM's
+ * (h, c)), whatever its len.  Sources are never destinations (by construction in
  * vs_beam_step), so the copy is hazard-free in place. */
 int vs_rows_copy(void* base, int64_t plane_stride_bytes, int32_t planes, int64_t row_stride_bytes,
                  int64_t pos_bytes, const int32_t* copy_list, const int32_t* n_copy,

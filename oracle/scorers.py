@@ -320,3 +320,75 @@ class TorchDecoderCPU:
         lg[self.eos] += self.eos_bias * T / enc.input_len
         peak = float(lg.max())
         return (lg - (peak + math.log(float(torch.exp(lg - peak).sum())))).numpy()
+
+
+class LSTMDecoderCPU:
+    """Reference-protocol scorer (bb/model.py:78-87: ``encode``, stateless
+    ``score_next``) for the configs[2] LSTM leg's CPU baseline: the random-init
+    model of paper_2010_02164_b200/decoder.py:LSTMScorer rebuilt on the CPU
+    from the same seeded generator sequence (the same bf16-rounded operands,
+    fp32 compute), re-running the decoder cell over the whole prefix for every
+    candidate as the reference's stateless protocol does.  Rows are the fp64
+    log-softmax of the logits (bb/model.py:216-217).  TEST/BASELINE
+    INFRASTRUCTURE: only tests/ and bench.py's cpu-baseline legs use it."""
+
+    HEADS, DH = 4, 64
+
+    def __init__(self, vocab_size: int, sos: int, eos: int, *, emb: int = 128, hidden: int = 256,
+                 seed: int = 0, tau: float = 4.0, eos_bias: float = 4.0):
+        import torch
+
+        self.torch = torch
+        self.vocab_size, self.sos, self.eos = vocab_size, sos, eos
+        self.H, self.tau, self.eos_bias = hidden, tau, eos_bias
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        V, E, H = vocab_size, emb, hidden
+
+        def w(*shape, std=None):  # same draw order / scaling as decoder.LSTMScorer
+            std = std if std is not None else 1.0 / math.sqrt(shape[-1])
+            return torch.randn(*shape, generator=g) * std
+
+        bf = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
+        p = {"emb": w(V, E, std=1.0), "enc_ih": w(4 * H, E), "enc_hh": w(4 * H, H), "enc_b": w(4 * H, std=0.1),
+             "dec_ih": w(4 * H, E), "dec_hh": w(4 * H, H), "dec_b": w(4 * H, std=0.1), "wc": w(H, 2 * H),
+             "out": w(V, H)}
+        self.emb = bf(p["emb"])
+        self.w_cell = bf(torch.cat([p["dec_ih"], p["dec_hh"]], 1))
+        self.b_cell = p["dec_b"]
+        self.wc = bf(p["wc"])
+        self.out_s = bf(p["out"] * tau)
+        self.encoder = torch.nn.LSTM(E, H, batch_first=True)
+        with torch.no_grad():
+            self.encoder.weight_ih_l0.copy_(p["enc_ih"])
+            self.encoder.weight_hh_l0.copy_(p["enc_hh"])
+            self.encoder.bias_ih_l0.copy_(p["enc_b"])
+            self.encoder.bias_hh_l0.zero_()
+        self._enc = {}
+
+    def encode(self, tokens, input_id: int = 0) -> Encoding:
+        torch = self.torch
+        toks = _check_input_tokens(tokens, self.vocab_size)
+        with torch.no_grad():
+            out, (h, c) = self.encoder(self.emb[list(toks)][None])
+        self._enc[(input_id, toks)] = (out[0].to(torch.bfloat16).float(), h[0, 0], c[0, 0])
+        return Encoding(input_id, toks, len(toks))
+
+    def score_next(self, enc: Encoding, cand):
+        torch = self.torch
+        out, h, c = self._enc[(enc.input_id, enc.tokens)]
+        bf = lambda t: t.to(torch.bfloat16).float()  # noqa: E731
+        with torch.no_grad():
+            for t in cand.tokens:
+                gates = torch.cat([self.emb[t], bf(h)]) @ self.w_cell.T + self.b_cell
+                i, f, gg, o = gates.chunk(4)
+                c = torch.sigmoid(f) * c + torch.sigmoid(i) * torch.tanh(gg)
+                h = torch.sigmoid(o) * torch.tanh(c)
+            q = bf(h).view(self.HEADS, self.DH)
+            k = out.view(-1, self.HEADS, self.DH)
+            a = torch.softmax(torch.einsum("hd,shd->hs", q, k) / 8.0, dim=-1)
+            ctx = bf(torch.einsum("hs,shd->hd", a, k).reshape(-1))
+            hb = bf(torch.tanh(torch.cat([bf(h), ctx]) @ self.wc.T))
+            lg = (hb @ self.out_s.T).double()
+        lg[self.eos] += self.eos_bias * len(cand.tokens) / enc.input_len
+        peak = float(lg.max())
+        return (lg - (peak + math.log(float(torch.exp(lg - peak).sum())))).numpy()

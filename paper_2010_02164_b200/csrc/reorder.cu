@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) rows_copy_kernel(unsigned char* __restric
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int c = it / planes, plane = it - c * planes;
     const int src = copy_list[3 * c], dst = copy_list[3 * c + 1], len = copy_list[3 * c + 2];
-    const int64_t bytes = (int64_t)len * pos_bytes;
+    const int64_t bytes = pos_bytes > 0 ? (int64_t)len * pos_bytes : -pos_bytes;  // < 0: fixed-size record
     const unsigned char* s = base + plane * plane_stride + (int64_t)src * row_stride;
     unsigned char* d = base + plane * plane_stride + (int64_t)dst * row_stride;
     if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d) | (uintptr_t)bytes) & 15) == 0) {
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(unsigned char* __rest
 extern "C" int vs_rows_copy(void* base, int64_t plane_stride_bytes, int32_t planes,
                             int64_t row_stride_bytes, int64_t pos_bytes, const int32_t* copy_list,
                             const int32_t* n_copy, int32_t max_copies, void* stream) {
-  if (!base || !copy_list || !n_copy || planes < 1 || planes > 65535 || pos_bytes < 1)
+  if (!base || !copy_list || !n_copy || planes < 1 || planes > 65535 || pos_bytes == 0)
     return VS_ERR_CONFIG;
   if (max_copies <= 0) return VS_OK;
   static int sms = 0;

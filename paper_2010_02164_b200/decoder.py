@@ -393,3 +393,211 @@ class GraphedTransformerScorer(TransformerScorer):
                                         kv.stride(2) * es, engine.t["copy_list"].data_ptr(),
                                         engine.t["n_copy"].data_ptr(), engine.max_copies, engine.stream_ptr),
                 "vs_rows_copy")
+
+
+class LSTMScorer:
+    """BASELINE.json configs[2]: the lightweight LSTM encoder-decoder parsing
+    shape (Dong & Lapata 2016 style): a 1-layer LSTM
+    encoder over the source, a 1-layer LSTM decoder cell whose state is
+    carried per PHYSICAL row, Luong dot attention over the slot's encoder
+    states (4 heads of 64 on the tensor-core grouped kernel: the rows of a
+    beam share their slot's states), h_att = tanh(W_c [h; ctx]) and logits
+    tau * h_att W_out^T plus the EOS bias eos_bias*len/src_len (the structure
+    of bb/model.py:215).  Random init (seeded), bf16 GEMM operands, fp32 cell
+    state and nonlinearities.
+
+    Per-row state (h, c) is a fixed-size record: extra children take a copy
+    of their parent's (K4 vs_rows_copy in fixed-size mode), first children
+    inherit the row.  A row of a freshly admitted beam (length 1) starts from
+    its slot's encoder final state.  The step is one CUDA graph per row
+    bucket (R from device memory, padded rows write a dummy row); the
+    encoder runs at admission (cuDNN) and its states are placed by K4's
+    vs_scatter_rows."""
+
+    host_sync = True
+    BUCKET = 128
+    HEADS, DH = 4, 64
+
+    def __init__(self, vocab: Vocabulary, *, emb: int = 128, hidden: int = 256, max_src: int = 128,
+                 seed: int = 0, tau: float = 4.0, eos_bias: float = 4.0, device=None, use_graphs: bool = True):
+        if hidden != self.HEADS * self.DH:
+            raise ValueError(f"LSTMScorer attention needs hidden = {self.HEADS * self.DH}")
+        if max_src > 256:
+            raise ValueError("LSTMScorer needs max_src <= 256 (grouped attention staging)")
+        self.vocab, self.E, self.H, self.max_src = vocab, emb, hidden, max_src
+        self.tau, self.eos_bias, self.use_graphs = float(tau), float(eos_bias), use_graphs
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        V, E, H = vocab.size, emb, hidden
+
+        def w(*shape, std=None):
+            std = std if std is not None else 1.0 / math.sqrt(shape[-1])
+            return torch.randn(*shape, generator=g) * std
+
+        self.params = {
+            "emb": w(V, E, std=1.0),
+            "enc_ih": w(4 * H, E), "enc_hh": w(4 * H, H), "enc_b": w(4 * H, std=0.1),
+            "dec_ih": w(4 * H, E), "dec_hh": w(4 * H, H), "dec_b": w(4 * H, std=0.1),
+            "wc": w(H, 2 * H), "out": w(V, H),
+        }
+        p = {k: v.to(self.device) for k, v in self.params.items()}
+        bf = torch.bfloat16
+        self.emb = p["emb"].to(bf)
+        self.w_cell = torch.cat([p["dec_ih"], p["dec_hh"]], 1).to(bf).contiguous()  # [4H, E+H]
+        self.b_cell = p["dec_b"].float()
+        self.wc = p["wc"].to(bf).contiguous()
+        self.out_s = (p["out"] * tau).to(bf).contiguous()  # tau folded, bf16 logits (K1 input)
+        self.encoder = torch.nn.LSTM(E, H, batch_first=True).to(self.device)
+        with torch.no_grad():
+            self.encoder.weight_ih_l0.copy_(p["enc_ih"])
+            self.encoder.weight_hh_l0.copy_(p["enc_hh"])
+            self.encoder.bias_ih_l0.copy_(p["enc_b"])
+            self.encoder.bias_hh_l0.zero_()
+        self.graphs, self.pool, self._bound = {}, None, None
+
+    graph_safe = False
+
+    def fork(self) -> "LSTMScorer":
+        import copy
+
+        other = copy.copy(self)
+        other.graphs, other.pool, other._bound = {}, None, None
+        return other
+
+    # ------------------------------------------------------------------ model
+    def encode_sources(self, src: torch.Tensor, lens: torch.Tensor):
+        """src [B, S] (padded), lens [B] -> (enc_out [B, S, H] bf16, h0, c0 [B, H] fp32)."""
+        x = self.emb[src].float()
+        packed = torch.nn.utils.rnn.pack_padded_sequence(x, lens.cpu(), batch_first=True, enforce_sorted=False)
+        with torch.no_grad():
+            out, (h, c) = self.encoder(packed)
+        out, _ = torch.nn.utils.rnn.pad_packed_sequence(out, batch_first=True, total_length=src.shape[1])
+        return out.to(torch.bfloat16), h[0], c[0]
+
+    def _cell(self, tok, h, c):
+        gates = (torch.cat([self.emb[tok], h.to(torch.bfloat16)], 1) @ self.w_cell.T).float() + self.b_cell
+        i, f, gg, o = gates.chunk(4, dim=1)
+        c2 = torch.sigmoid(f) * c + torch.sigmoid(i) * torch.tanh(gg)
+        h2 = torch.sigmoid(o) * torch.tanh(c2)
+        return h2, c2
+
+    def _head(self, h, ctx, ln, src_len):
+        hb = torch.tanh((torch.cat([h.to(torch.bfloat16), ctx], 1) @ self.wc.T).float()).to(torch.bfloat16)
+        lg = hb @ self.out_s.T
+        eos = self.vocab.eos
+        lg[:, eos] = (lg[:, eos].float() + self.eos_bias * ln.float() / src_len).to(torch.bfloat16)
+        return lg
+
+    def full_forward(self, src_tokens, prefix):
+        """Cache-free logits of the last position of `prefix` (tests)."""
+        dev = self.device
+        src = torch.tensor([list(src_tokens)], device=dev)
+        enc, h, c = self.encode_sources(src, torch.tensor([len(src_tokens)]))
+        for t in prefix:
+            h, c = self._cell(torch.tensor([t], device=dev), h, c)
+        q = h.to(torch.bfloat16).view(1, self.HEADS, self.DH).float()
+        k = enc[0].float().view(-1, self.HEADS, self.DH)
+        a = torch.softmax(torch.einsum("hd,shd->hs", q[0], k) / 8.0, dim=-1)
+        ctx = torch.einsum("hs,shd->hd", a, k).reshape(1, -1).to(torch.bfloat16)
+        return self._head(h, ctx, torch.tensor([len(prefix)], device=dev),
+                          torch.tensor([float(len(src_tokens))], device=dev))[0].float()
+
+    # --------------------------------------------------------- engine protocol
+    def bind(self, engine) -> None:
+        n, k, dev = engine.n, engine.k, engine.device
+        key = (id(engine), n, k, engine.capacity)
+        if self._bound != key:  # graphs capture these buffers
+            self.engine = engine
+            self.dummy = n * k
+            self.state = torch.zeros(n * k + 1, 2, self.H, device=dev, dtype=torch.float32)
+            self.enc = torch.zeros(n, self.max_src, self.H, device=dev, dtype=torch.bfloat16)
+            self.enc_hc = torch.zeros(n, 2, self.H, device=dev, dtype=torch.float32)
+            self.enc_len = torch.zeros(n, dtype=torch.int32, device=dev)
+            ld = (self.vocab.size + 7) // 8 * 8
+            self.lg = torch.empty(engine.capacity, ld, device=dev, dtype=torch.bfloat16)
+            self.graphs, self.pool, self._bound = {}, None, key
+        self.enc_len.zero_()
+        self._corpus_off = engine.t["src_off"].cpu().numpy()
+        self._corpus_tok = engine.t["src_tok"].cpu().numpy()
+
+    def on_admit(self, engine, status) -> None:
+        n = engine.n
+        a0, na = int(status[N.ST_ADMIT0]), int(status[N.ST_NADMIT])
+        slots = torch.tensor(status[N.ST_HDR + 3 * n:N.ST_HDR + 3 * n + na].astype("int32"), device=engine.device)
+        srcs = [self._corpus_tok[self._corpus_off[i]:self._corpus_off[i + 1]] for i in range(a0, a0 + na)]
+        lens = torch.tensor([len(s_) for s_ in srcs])
+        S = int(lens.max())
+        if S > self.max_src:
+            raise ValueError("source longer than the encoder's max_src")
+        pad = torch.zeros(na, S, dtype=torch.long)
+        for i, s_ in enumerate(srcs):
+            pad[i, : len(s_)] = torch.from_numpy(s_.astype("int64"))
+        out, h, c = self.encode_sources(pad.to(engine.device), lens)
+        hc = torch.stack([h, c], 1).contiguous()
+        lib, st = engine.lib, engine.stream_ptr
+        # K4, encoder half: each admitted source's states into its slot
+        N.check(lib.vs_scatter_rows(self.enc.data_ptr(), self.enc.stride(0) * 2, out.data_ptr(), out.stride(0) * 2,
+                                    S * self.H * 2, slots.data_ptr(), None, na, st), "vs_scatter_rows")
+        N.check(lib.vs_scatter_rows(self.enc_hc.data_ptr(), self.enc_hc.stride(0) * 4, hc.data_ptr(),
+                                    hc.stride(0) * 4, hc.stride(0) * 4, slots.data_ptr(), None, na, st),
+                "vs_scatter_rows")
+        self.enc_len[slots.long()] = lens.to(engine.device, torch.int32)
+
+    def _body(self, Rb: int):
+        eng, t = self.engine, self.engine.t
+        Lmax = eng.max_len
+        R = t["status"][N.ST_R]
+        valid = torch.arange(Rb, device=self.device, dtype=torch.int32) < R
+        phys = torch.where(valid, t["row_phys"][:Rb], 0).long()
+        slot = torch.where(valid, t["row_slot"][:Rb], 0).to(torch.int32)
+        ln = torch.where(valid, t["row_len"][:Rb], 1)
+        tok = t["hist"].view(-1, Lmax)[phys, (ln - 1).long()].long()
+        fresh = (ln == 1)[:, None]
+        prev = torch.where(fresh[:, :, None], self.enc_hc[slot.long()], self.state[phys])
+        h, c = self._cell(tok, prev[:, 0], prev[:, 1])
+        self.state[torch.where(valid, phys, self.dummy)] = torch.stack([h, c], 1)
+        q = h.to(torch.bfloat16).contiguous()
+        ctx = torch.empty(Rb, self.H, device=self.device, dtype=torch.bfloat16)
+        enc_len = self.enc_len[slot.long()]
+        N.check(eng.lib.vs_row_attention_grouped(
+            q.data_ptr(), q.stride(0), self.enc.data_ptr(), self.enc.data_ptr(), self.enc.stride(0),
+            self.enc.stride(1), slot.data_ptr(), enc_len.data_ptr(), t["sel_off"].data_ptr(),
+            eng.status_ptr(N.ST_NSEL), eng.n, ctx.data_ptr(), ctx.stride(0), self.HEADS, self.DH, 1.0 / 8.0,
+            torch.cuda.current_stream(self.device).cuda_stream), "vs_row_attention_grouped")
+        src_len = t["slot_src_len"][slot.long()].float()
+        self.lg[:Rb, : self.vocab.size] = self._head(h, ctx, ln, src_len)
+
+    def logits(self, engine, R):
+        if R is None:
+            raise RuntimeError("LSTMScorer needs the synchronous driver")
+        if R == 0:
+            return self.lg, N.VS_DTYPE_BF16
+        Rb = min((R + self.BUCKET - 1) // self.BUCKET * self.BUCKET, engine.capacity)
+        if not self.use_graphs:
+            self._body(Rb)
+            return self.lg, N.VS_DTYPE_BF16
+        g = self.graphs.get(Rb)
+        if g is None:
+            saved = self.state.clone()
+            s = torch.cuda.Stream(self.device)
+            s.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(s):
+                self._body(Rb)  # warm-up
+            torch.cuda.current_stream(self.device).wait_stream(s)
+            self.state.copy_(saved)  # the warm-up advanced the rows' state once
+            g = torch.cuda.CUDAGraph()
+            if self.pool is None:
+                self.pool = torch.cuda.graph_pool_handle()
+            with torch.cuda.graph(g, pool=self.pool, capture_error_mode="thread_local"):
+                self._body(Rb)
+            self.state.copy_(saved)
+            self.graphs[Rb] = g
+        g.replay()
+        return self.lg, N.VS_DTYPE_BF16
+
+    def after_step(self, engine, R) -> None:
+        # K4 in fixed-size mode: each planned copy moves the parent's whole (h, c) record
+        st = self.state
+        N.check(engine.lib.vs_rows_copy(st.data_ptr(), 0, 1, st.stride(0) * 4, -(st.stride(0) * 4),
+                                        engine.t["copy_list"].data_ptr(), engine.t["n_copy"].data_ptr(),
+                                        engine.max_copies, engine.stream_ptr), "vs_rows_copy")

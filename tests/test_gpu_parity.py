@@ -845,3 +845,49 @@ def test_api_per_beam_and_batch_pieces_reproduce_reference():
         g = A.greedy_decode(enc, sc, cfg.max_len)
         og = O.greedy_decode(enc, base, cfg.max_len)
         assert (g.tokens, g.score) == (og.tokens, og.score)
+
+
+def _lstm_run(use_graphs=True, k=6, n=8, N_in=48):
+    P, N, SearchEngine, _, _, LseRecorder = _pkg()
+    from paper_2010_02164_b200.decoder import LSTMScorer
+
+    vocab = P.Vocabulary(700, 0, 2)
+    cfg = P.DecodeConfig(k=k, n=n, epsilon=1 / 4, delta=3.0, max_candidates=3, max_len=20)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(8, N_in, 700, mean_len=7.0, clip=40))
+    dec = LSTMScorer(vocab, emb=64, hidden=256, max_src=64, seed=2, tau=3.0, eos_bias=4.0, use_graphs=use_graphs)
+    rec = LseRecorder(dec, record_logits=True)
+    ev = []
+    out, rep = P.run_varstream(corpus, rec, cfg, trace=True, on_step=ev.append)
+    return P, vocab, cfg, corpus, dec, rec, ev, out, rep
+
+
+def test_lstm_scorer_state_reorder_matches_full_recompute():
+    """configs[2]'s LSTM decoder: the per-physical-row (h, c) state, moved by
+    K4 in fixed-size mode from K2's copy plan, and the grouped tensor-core
+    attention over the slot's encoder states reproduce a cache-free forward
+    of sampled prefixes (bf16 operands: tolerance 0.05 + 2% of the scale)."""
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _lstm_run()
+    keys = sorted(rec.logit_table)
+    rng = np.random.default_rng(3)
+    sample = [keys[i] for i in rng.choice(len(keys), size=min(40, len(keys)), replace=False)]
+    sample += sorted(keys, key=lambda kk: -len(kk[1]))[:10]
+    worst = 0.0
+    for iid, toks in sample:
+        want = dec.full_forward(corpus[iid], toks).cpu().numpy()
+        got = rec.logit_table[(iid, toks)]
+        worst = max(worst, float(np.max(np.abs(got - want))) / (0.05 + 0.02 * float(np.max(np.abs(want)))))
+    assert worst <= 1.0, worst
+
+
+def test_lstm_scorer_decisions_match_oracle_replay_and_eager():
+    from oracle.scorers import RecordedRowsScorer
+
+    P, vocab, cfg, corpus, dec, rec, ev, out, rep = _lstm_run()
+    assert len(dec.graphs) >= 1
+    cpu = RecordedRowsScorer(vocab.size, vocab.sos, vocab.eos, rec.logit_table, rec.table)
+    oev = []
+    want, wrep = O.run_varstream(corpus, cpu, O.as_oconfig(cfg), trace=True, on_step=oev.append)
+    assert _events(ev) == _events(oev)
+    assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
+    *_, out2, rep2 = _lstm_run(use_graphs=False)
+    assert [[(c.tokens, c.score) for c in per] for per in out2] == [[(c.tokens, c.score) for c in per] for per in out]
