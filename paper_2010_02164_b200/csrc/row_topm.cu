@@ -351,6 +351,7 @@ __device__ __forceinline__ float tl_seed(TopList<K>& t, float lm, int lt, int Me
 // wave quantisation against the per-warp fixed cost.
 __host__ __device__ __forceinline__ int pick_w(int R, int V, int T, float c0 = PICKW_C0) {
   if (V < 4096 || R <= 0) return 1;
+  if (c0 < 0.0f) return min(WPC, (int)(-c0));  // VS_K1_C0=-W pins W (measurement knob)
   int best = 1;
   float bc = 1e30f, inv = 1.0f;  // 32-bit unsigned math: this runs in every warp's prologue
   for (int w = 1; w <= WPC; w <<= 1, inv *= 0.5f) {
