@@ -441,6 +441,101 @@ def _dec_cpu_worker(args):
     return time.perf_counter() - t0, rep.candidate_expansions
 
 
+def _dec_agree_worker(args):
+    """Spawned process: reference search + CPU transformer on a few inputs;
+    returns their outputs and, for the ones listed in `margins_for`, the
+    reference's smallest decision margin (oracle/agreement.py)."""
+    w, items, weights = args
+    import torch
+
+    torch.set_num_threads(1)
+    from oracle import varstream_oracle as O
+    from oracle.agreement import decode_with_margin
+    from oracle.scorers import TorchDecoderCPU
+
+    sc = TorchDecoderCPU(w["V"], w["sos"], w["eos"], seed=0, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, weights=weights)
+    sc.incremental = True  # per-prefix K/V cache, a beam's rows in one batch: the same model
+    cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                    max_len=w["max_len"])
+    out = []
+    for gid, toks in items:
+        enc = sc.encode(toks, input_id=gid)
+        got, margin = decode_with_margin(enc, sc, cfg)  # bb/search.py:233-242: batch-independent
+        out.append((gid, [(c.tokens, c.score) for c in got], margin))
+    return out
+
+
+def decoder_agreement(w, n_inputs: int = 64, procs: int | None = None, precision: str = "bf16"):
+    """north_star's end-to-end agreement on the WMT'19 decoder: the device
+    decode (bf16 transformer-big, graphed, cuBLAS head) vs the reference
+    search driving the same random-init weights on the CPU
+    (oracle/scorers.py:TorchDecoderCPU, fp32 compute on the bf16 weights,
+    fp64 rows) on n_inputs evenly strided inputs.  Reports the identical and
+    top-1 fractions and, per divergent input, the reference's own smallest
+    decision margin (an fp near-tie when it is below the bf16-vs-fp32 logit
+    discrepancy).  precision="fp32" runs the same model in fp32 on the device
+    (decoder.TransformerScorer, TF32 off; n=8 slots to bound the fp32 K/V
+    cache — outputs do not depend on n) against fp32 weights on the CPU: the
+    search itself, on the real model shape, with matching arithmetic."""
+    import multiprocessing as mp
+
+    import torch
+
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
+    from paper_2010_02164_b200.decoder import GraphedTransformerScorer, TransformerScorer
+    from oracle.agreement import compare
+
+    corpus = _corpus(w)
+    stride = max(1, len(corpus) // n_inputs)
+    ids = list(range(stride // 2, len(corpus), stride))[:n_inputs]
+    sample = [corpus[i] for i in ids]
+    vocab = Vocabulary(w["V"], w["sos"], w["eos"])
+    cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                       max_len=w["max_len"])
+    if precision == "fp32":
+        cfg = DecodeConfig(k=w["k"], n=8, epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                           max_len=w["max_len"])
+        dec = TransformerScorer(vocab, d=1024, heads=16, layers=6, enc_layers=6, ffn=4096, max_src=256, seed=0,
+                                tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, dtype=torch.float32)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            gpu, _ = run_varstream(sample, dec, cfg)
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        del dec
+        torch.cuda.empty_cache()
+    else:
+        dec = GraphedTransformerScorer(vocab, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0)
+        gpu, _ = run_varstream(sample, dec, cfg)
+    weights = "f32" if precision == "fp32" else "bf16"
+    # the logit discrepancy of the two implementations on the rows the device scored
+    procs = procs or min(len(sample), os.cpu_count() or 1, 64)
+    chunks = [[(q, sample[q]) for q in range(p, len(sample), procs)] for p in range(procs)]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(procs) as pool:
+        res = [r for part in pool.map(_dec_agree_worker, [(w, c, weights) for c in chunks]) for r in part]
+    wall = time.perf_counter() - t0
+    same = top1 = 0
+    div = []
+    for q, want, margin in sorted(res):
+        got = [(c.tokens, c.score) for c in gpu[q]]
+        s_, t_ = compare(got, want)
+        same += s_
+        top1 += t_
+        if not s_:
+            div.append({"input": ids[q], "top1_same": bool(t_), "reference_margin": float(f"{margin:.3g}")})
+    n = len(sample)
+    return {"inputs": n, "precision": precision, "identical_fraction": round(same / n, 4),
+            "top1_fraction": round(top1 / n, 4), "divergent": len(div), "divergences": div,
+            "device_model": "GraphedTransformerScorer, bf16 (the bench leg's model)" if precision == "bf16" else
+                            "TransformerScorer fp32 (TF32 off), same weights",
+            "reference": "oracle beam_decode (bb/search.py:233-242) + TorchDecoderCPU (same random-init weights"
+                         + (" rounded to bf16" if precision == "bf16" else ", fp32") +
+                         ", fp32 compute, fp64 log-softmax rows)",
+            "sample": f"{n} inputs, every {stride}th of the length-sorted corpus", "cpu_wall_s": round(wall, 1)}
+
+
 def decoder_cpu_baseline(w, procs: int = 8):
     """The reference search + CPU transformer scorer on host cores: `procs`
     single-threaded processes, one input each, evenly strided over the
@@ -702,6 +797,8 @@ def run_ours(args):
         line["decoder_wmt19_k5"] = decoder_leg(w, args.decoder_inputs, fused_head=True, batches=3)
         if args.decoder_cpu_baseline:  # ~3.5 min of host time: opt-in
             line["decoder_wmt19"]["cpu_baseline"] = decoder_cpu_baseline(w)
+        if args.decoder_agreement:  # minutes of host time: opt-in (profiles/round2/decoder_agreement.json)
+            line["decoder_wmt19"]["reference_agreement"] = decoder_agreement(w, args.decoder_agreement)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, txt, _, cpu_outs = cpu_reference(w, local_corpus, per_proc=args.cpu_per_proc)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "seq/s", "cores": cores, "kind": "port",
@@ -764,6 +861,8 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: N inputs per rank; strong: --strong-n inputs over all ranks (configs[4])")
     ap.add_argument("--strong-n", type=int, default=100000)
+    ap.add_argument("--decoder-agreement", type=int, default=0,
+                    help="also compare N strided decoder-leg inputs with the reference search on the CPU model")
     ap.add_argument("--decoder-inputs", type=int, default=10000,
                     help="inputs for the transformer-big decoder leg (0 = skip)")
     args = ap.parse_args()

@@ -43,11 +43,21 @@ def compare(got, want, rel: float = 1e-5):
 def decision_margin(encoding, scorer, cfg: O.OConfig) -> float:
     """Smallest decision margin of the reference's deferred-policy search for
     one input (see module docstring)."""
+    return decode_with_margin(encoding, scorer, cfg)[1]
+
+
+def decode_with_margin(encoding, scorer, cfg: O.OConfig):
+    """The reference's unbatched search of one input (bb/search.py:233-242)
+    and its smallest decision margin, in one pass: (outputs, margin)."""
     beam = O.Beam.initial(encoding.input_id, scorer.sos)
     margin = math.inf
+    outputs = []
     while True:
         actives = [(i, c) for i, c in enumerate(beam.candidates) if not c.finalized]
-        rows = [np.asarray(scorer.score_next(encoding, c), dtype=np.float64) for _, c in actives]
+        if getattr(scorer, "incremental", False) and actives:  # the same rows, one batched model pass
+            rows = [np.asarray(r, dtype=np.float64) for r in scorer.score_batch(encoding, [c for _, c in actives])]
+        else:
+            rows = [np.asarray(scorer.score_next(encoding, c), dtype=np.float64) for _, c in actives]
         for row in rows:
             m = min(cfg.max_candidates, row.shape[0])
             if m < row.shape[0]:
@@ -64,10 +74,12 @@ def decision_margin(encoding, scorer, cfg: O.OConfig) -> float:
                 margin = min(margin, abs(p.score - cutoff))
         nxt, emitted = O.expand_beam(beam, rows, cfg, scorer.vocab_size, scorer.eos)
         if nxt.l_t >= cfg.max_len and nxt.candidates:
-            nxt, _ = O.drain_at_length_cap(nxt, cfg)
+            nxt, drained = O.drain_at_length_cap(nxt, cfg)
+            emitted = emitted + drained
+        outputs += emitted
         beam = nxt
         if O.beam_finished(beam, cfg):
-            return margin
+            return outputs, margin
 
 
 def agreement_report(corpus, ids, gpu_sig, cpu_sig, scorer, cfg: O.OConfig, tie_tol: float,

@@ -303,6 +303,8 @@ class TorchDecoderCPU:
         return enc
 
     def score_next(self, enc: Encoding, cand):
+        if getattr(self, "incremental", False):
+            return self.score_batch(enc, [cand])[0]
         torch, F = self.torch, self.torch.nn.functional
         cross = self._cross[(enc.input_id, enc.tokens)]
         prefix = list(cand.tokens)
@@ -321,6 +323,58 @@ class TorchDecoderCPU:
         peak = float(lg.max())
         return (lg - (peak + math.log(float(torch.exp(lg - peak).sum())))).numpy()
 
+
+    def score_batch(self, enc: Encoding, cands):
+        """Incremental mode: rows for several candidates of one beam (all of one
+        length) in one batched pass per layer and one vocab GEMM, with each
+        prefix's per-layer K/V cached by token tuple (a candidate's parent
+        holds positions 0..T-2).  The model is unchanged; only the fp32
+        evaluation order differs from whole-prefix recompute."""
+        import collections
+
+        torch, F = self.torch, self.torch.nn.functional
+        if not hasattr(self, "_kv"):
+            self._kv = collections.OrderedDict()
+        if len({len(c.tokens) for c in cands}) != 1:
+            return [r for c in cands for r in self.score_batch(enc, [c])]
+        cross = self._cross[(enc.input_id, enc.tokens)]
+        T = len(cands[0].tokens)
+        parents = []
+        for c in cands:
+            key = (enc.input_id, tuple(c.tokens[:-1]))
+            if T > 1 and key not in self._kv:  # not cached: build the prefix first
+
+                class _P:
+                    tokens = tuple(c.tokens[:-1])
+
+                self.score_batch(enc, [_P])
+            parents.append(self._kv[key] if T > 1 else None)
+        d, B = self.d, len(cands)
+        with torch.no_grad():
+            x = (self.emb[[c.tokens[-1] for c in cands]] + self.pos[T - 1])[:, None]  # [B, 1, d]
+            per_row = [[] for _ in range(B)]
+            for li, (L, (ck, cv)) in enumerate(zip(self.dec, cross)):
+                q, k, v = (x @ L["qkv"].T).split(d, dim=-1)
+                if T > 1:
+                    K = torch.cat([torch.stack([p[li][0] for p in parents]), k], 1)
+                    Vv = torch.cat([torch.stack([p[li][1] for p in parents]), v], 1)
+                else:
+                    K, Vv = k, v
+                for b in range(B):
+                    per_row[b].append((K[b], Vv[b]))
+                x = F.layer_norm(x + self._attn(q, K, Vv, None) @ L["o"].T, (d,))
+                x = F.layer_norm(x + self._attn(x @ L["cq"].T, ck.expand(B, -1, -1), cv.expand(B, -1, -1), None)
+                                 @ L["co"].T, (d,))
+                x = F.layer_norm(x + F.gelu(x @ L["f1"].T) @ L["f2"].T, (d,))
+            lg = x[:, 0] @ self.out_s.T
+            lg = (lg * self.post_tau if self.post_tau != 1.0 else lg).double()
+        for b, c in enumerate(cands):
+            self._kv[(enc.input_id, tuple(c.tokens))] = per_row[b]
+        while len(self._kv) > 512:
+            self._kv.popitem(last=False)
+        lg[:, self.eos] += self.eos_bias * T / enc.input_len
+        peak = lg.max(dim=1, keepdim=True).values
+        return list((lg - (peak + torch.log(torch.exp(lg - peak).sum(dim=1, keepdim=True)))).numpy())
 
 class LSTMDecoderCPU:
     """Reference-protocol scorer (bb/model.py:78-87: ``encode``, stateless

@@ -53,3 +53,44 @@ def test_torch_decoder_cpu_f32_is_the_product_model():
     lg = prod.full_forward(src, C.tokens).double()
     want = (lg - torch.logsumexp(lg, 0)).numpy()
     assert np.max(np.abs(row - want)) < 1e-4
+
+
+def test_torch_decoder_cpu_incremental_matches_full_recompute():
+    """The CPU reference model's per-prefix K/V cache (used for the decoder
+    agreement run) computes the same rows as whole-prefix recompute."""
+    from oracle.scorers import TorchDecoderCPU
+
+    kw = dict(d=32, heads=4, layers=2, enc_layers=1, ffn=64, seed=3, tau=3.0, eos_bias=3.0)
+    full = TorchDecoderCPU(97, 0, 2, **kw)
+    inc = TorchDecoderCPU(97, 0, 2, **kw)
+    inc.incremental = True
+
+    class C:
+        def __init__(self, tokens, score=0.0, finalized=False, input_id=0):
+            self.tokens = tokens
+
+    src = [5, 6, 7, 8]
+    e1, e2 = full.encode(src, 0), inc.encode(src, 0)
+    for pre in [(0,), (0, 9), (0, 9, 4), (0, 9, 4, 11), (0, 12)]:
+        a, b = full.score_next(e1, C(pre)), inc.score_next(e2, C(pre))
+        assert np.max(np.abs(a - b)) < 1e-4
+
+
+def test_torch_decoder_cpu_score_batch_matches_rows():
+    from oracle.scorers import TorchDecoderCPU
+
+    kw = dict(d=32, heads=4, layers=2, enc_layers=1, ffn=64, seed=3, tau=3.0, eos_bias=3.0)
+    a = TorchDecoderCPU(97, 0, 2, **kw)
+    b = TorchDecoderCPU(97, 0, 2, **kw)
+    b.incremental = True
+
+    class C:
+        def __init__(self, tokens):
+            self.tokens = tokens
+
+    e1, e2 = a.encode([5, 6, 7], 0), b.encode([5, 6, 7], 0)
+    b.score_batch(e2, [C((0,))])
+    b.score_batch(e2, [C((0, 9)), C((0, 4))])
+    got = b.score_batch(e2, [C((0, 9, 1)), C((0, 4, 7)), C((0, 9, 3))])
+    for g, t in zip(got, [(0, 9, 1), (0, 4, 7), (0, 9, 3)]):
+        assert np.max(np.abs(g - a.score_next(e1, C(t)))) < 1e-4
