@@ -199,11 +199,14 @@ class SearchEngine:
         self._bufs = {}    # grow-only corpus / output buffers
         self._forks = {}   # scorer forks bound to this engine (concurrent batches)
         self._graphs, self._graph_key, self._graph_scorer = None, None, None
+        self._sp = None    # stream pinned by the running driver
 
     # ------------------------------------------------------------------ data
     @property
     def stream_ptr(self) -> int:
-        return torch.cuda.current_stream(self.device).cuda_stream
+        # the drivers pin the stream for their launches (one query per step, not per call)
+        sp = self._sp
+        return sp if sp is not None else torch.cuda.current_stream(self.device).cuda_stream
 
     def load_corpus(self, corpus, *, src_tok=None, src_off=None) -> None:
         """Copy the (length-bucketed) input stream to HBM and size the outputs.
@@ -355,9 +358,18 @@ class SearchEngine:
         The schedule that opens iteration t+1 (removal of step t's finished
         beams, flush check, refill, selection) runs inside step t's fused
         beam-step launch, so the host decides its modes before launching."""
+        self._sp = None
         cfgd = self.config
         self.load_corpus(corpus)
         scorer.bind(self)
+        self._sp = torch.cuda.current_stream(self.device).cuda_stream
+        try:
+            return self._run(scorer, admit_mode, select_mode, flush_enabled, trace, on_step)
+        finally:
+            self._sp = None
+
+    def _run(self, scorer, admit_mode, select_mode, flush_enabled, trace, on_step):
+        cfgd = self.config
         report = MetricsReport.new(trace=trace)
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
         n = self.n
@@ -431,6 +443,7 @@ class SearchEngine:
         With ``harvest_into`` (a list indexed by global input id; ``gids`` maps
         this engine's inputs to global ids) the outputs are streamed to the
         host while the device decodes (``Harvest``)."""
+        self._sp = None
         cfgd = self.config
         self.load_corpus(corpus, src_tok=src_tok, src_off=src_off)
         scorer.bind(self)
@@ -471,6 +484,7 @@ class SearchEngine:
             if done:
                 break
             stream = torch.cuda.current_stream(self.device)
+            self._sp = stream.cuda_stream
             if graphs is not None:
                 graphs[(launched // spg) % len(graphs)].replay()
             else:
@@ -492,6 +506,7 @@ class SearchEngine:
             launched += spg
             yield
         self.launched_steps = launched
+        self._sp = None
         st = self.read_status()
         if st[N.ST_CURSOR] != self.N:
             raise InvariantViolation(f"run consumed {int(st[N.ST_CURSOR])} of {self.N} inputs")
