@@ -852,7 +852,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-per-proc", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=6,
                     help="concurrent refilling batches (n slots each) per GPU, on separate CUDA streams")
     ap.add_argument("--decoder-cpu-baseline", action="store_true",
                     help="also time the reference search + CPU transformer scorer (8 inputs, ~3.5 min)")

@@ -119,11 +119,19 @@ class Harvest:
 
     def _materialize(self, lo, count, lens, scores, offs) -> None:
         out, gids, toks, k = self.out, self.gids, self.toks, self.eng.k
+        new, sa, C = object.__new__, object.__setattr__, Candidate  # inlined _candidate (hot loop)
         for q, cnt in enumerate(count):
             gi = lo + q if gids is None else int(gids[lo + q])
-            b = q * k
-            out[gi] = [_candidate(tuple(toks[offs[e]:offs[e] + lens[e]]), scores[e], gi)
-                       for e in range(b, b + cnt)]
+            per = []
+            for e in range(q * k, q * k + cnt):
+                o = offs[e]
+                c = new(C)
+                sa(c, "tokens", tuple(toks[o:o + lens[e]]))
+                sa(c, "score", scores[e])
+                sa(c, "finalized", True)
+                sa(c, "input_id", gi)
+                per.append(c)
+            out[gi] = per
 
     def finish(self, st) -> list:
         """After the run's final status (synchronised): request the rest, wait."""

@@ -175,11 +175,9 @@ def run_varstream_sharded(corpus, scorer, config, *, group=None, dst: int = 0, s
         for st, _ in jobs:
             if st is not None:
                 torch.cuda.current_stream().wait_stream(st)
-        rep = reps[0]
-        for r_ in reps[1:]:
-            rep.timesteps += r_.timesteps
-            rep.candidate_expansions += r_.candidate_expansions
-            rep.simulated_cost += r_.simulated_cost
+        from .metrics import merge_reports
+
+        rep = merge_reports(reps)
         packed = merge_packs([e.packed() for e in engs], subs, len(local))
     elif local:
         eng = SearchEngine(config, _vocab(scorer))

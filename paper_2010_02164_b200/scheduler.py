@@ -18,7 +18,7 @@ from .core import Candidate, DecodeConfig, Vocabulary
 from .engine import SearchEngine, drive_concurrent
 from .errors import ConfigError
 from .harness import shard
-from .metrics import CostParams, MetricsReport
+from .metrics import CostParams, MetricsReport, merge_reports
 from .scorers import HostScorerAdapter
 
 ENGINES = ("greedy", "fixed", "varbeam", "varstream", "varfifo", "fixedstream")
@@ -79,14 +79,8 @@ def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
         engines.append(eng)
         jobs.append((stream, gen))
     reports = drive_concurrent(jobs)
-    merged = MetricsReport.new(trace=trace)
-    for rep in reports:
-        merged.timesteps += rep.timesteps
-        merged.candidate_expansions += rep.candidate_expansions
-        merged.simulated_cost += rep.simulated_cost
-        if trace and rep.per_step_trace:
-            merged.per_step_trace.extend(rep.per_step_trace)
-    return out, merged
+    # counters summed over the batches; trace renumbered (metrics.merge_reports)
+    return out, merge_reports(reports, trace)
 
 
 def _run(corpus, scorer, config, admit, select, flush, trace, on_step, fast, streams=1):

@@ -78,3 +78,18 @@ def test_refill_and_selection_match_oracle():
         assert (sel.total_expansions, sel.effective_len) == (total, eff)
     with pytest.raises(ConfigError):
         A.select_min_lt(st, 2)
+
+
+def test_merge_reports_sums_counters_and_renumbers_trace():
+    from paper_2010_02164_b200.metrics import CostParams, MetricsReport, merge_reports
+
+    a, b = MetricsReport.new(trace=True), MetricsReport.new(trace=True)
+    cp = CostParams(1.0, 1.0)
+    for r, steps in ((a, [(4, 1), (6, 2)]), (b, [(3, 1), (5, 2), (2, 3)])):
+        for e, L in steps:
+            r.record_step(e, L, cp)
+    m = merge_reports([a, b], trace=True)
+    assert (m.timesteps, m.candidate_expansions) == (5, 20)
+    assert m.simulated_cost == a.simulated_cost + b.simulated_cost
+    assert [r.timestep for r in m.per_step_trace] == [1, 2, 3, 4, 5]
+    assert [(r.expansions, r.effective_len) for r in m.per_step_trace] == [(4, 1), (6, 2), (3, 1), (5, 2), (2, 3)]
