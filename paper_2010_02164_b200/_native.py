@@ -112,6 +112,29 @@ def load_library(path: Path | None = None) -> C.CDLL:
     return lib
 
 
+_vsmat = None
+
+
+def load_vsmat():
+    """The host-runtime extension (_lib/_vsmat*.so, built by __graft_entry__.build())
+    that materialises decode outputs as Candidate lists in bulk."""
+    global _vsmat
+    if _vsmat is None:
+        import importlib.machinery
+        import importlib.util
+        import sysconfig
+
+        p = LIB_PATH.parent / ("_vsmat" + sysconfig.get_config_var("EXT_SUFFIX"))
+        if not p.exists():
+            raise RuntimeError(f"host extension not built: {p} (run __graft_entry__.build())")
+        loader = importlib.machinery.ExtensionFileLoader("_vsmat", str(p))
+        spec = importlib.util.spec_from_loader("_vsmat", loader)
+        mod = importlib.util.module_from_spec(spec)
+        loader.exec_module(mod)
+        _vsmat = mod
+    return _vsmat
+
+
 def check(rc: int, what: str) -> None:
     """Map a C-ABI status onto the reference taxonomy (bb/errors.py)."""
     if rc == VS_OK:

@@ -84,7 +84,11 @@ class Harvest:
         self.eng, self.out, self.gids, self.chunk = eng, out, gids, chunk
         self.lo = 0          # inputs [0, lo) requested
         self.tok_hi = 0      # out_tok[0, tok_hi) requested
-        self.toks: list = []  # host copy of out_tok[0, tok_hi), as Python ints
+        self.toks = np.empty(1 << 16, dtype=np.int32)  # host copy of out_tok[0, landed)
+        self.landed = 0
+        self.gids_np = None if gids is None else np.ascontiguousarray(np.asarray(gids), dtype=np.int64)
+        self.mat = N.load_vsmat()
+        self.mat.reserve(eng.vocab.size)
         self.pending = []
         self.d2h_bytes = 0
 
@@ -112,26 +116,17 @@ class Harvest:
         while self.pending and (block or self.pending[0][0].query()):
             ev, lo, hi, host = self.pending.pop(0)
             ev.synchronize()
-            count, lens, scores, offs, tok = host
-            self.toks.extend(tok.numpy().tolist())
-            self._materialize(lo, count.numpy().tolist(), lens.numpy().tolist(), scores.numpy().tolist(),
-                              offs.numpy().tolist())
-
-    def _materialize(self, lo, count, lens, scores, offs) -> None:
-        out, gids, toks, k = self.out, self.gids, self.toks, self.eng.k
-        new, sa, C = object.__new__, object.__setattr__, Candidate  # inlined _candidate (hot loop)
-        for q, cnt in enumerate(count):
-            gi = lo + q if gids is None else int(gids[lo + q])
-            per = []
-            for e in range(q * k, q * k + cnt):
-                o = offs[e]
-                c = new(C)
-                sa(c, "tokens", tuple(toks[o:o + lens[e]]))
-                sa(c, "score", scores[e])
-                sa(c, "finalized", True)
-                sa(c, "input_id", gi)
-                per.append(c)
-            out[gi] = per
+            count, lens, scores, offs, tok = (h.numpy() for h in host)
+            end = self.landed + tok.shape[0]
+            if end > self.toks.shape[0]:
+                grown = np.empty(max(end, 2 * self.toks.shape[0]), dtype=np.int32)
+                grown[: self.landed] = self.toks[: self.landed]
+                self.toks = grown
+            self.toks[self.landed:end] = tok
+            self.landed = end
+            # C: Candidate objects with their slots filled directly (hostsrc/vsmat.c)
+            self.mat.fill(self.out, self.gids_np, lo, count, lens, scores, offs, self.toks[:end], self.eng.k,
+                          Candidate)
 
     def finish(self, st) -> list:
         """After the run's final status (synchronised): request the rest, wait."""

@@ -96,19 +96,18 @@ def deserialize_pack(buf: np.ndarray):
 
 
 def materialize(out: list, gids, count, lens, scores, toks) -> None:
-    """Candidate lists of a packed shard into `out` at global ids `gids`."""
-    from .engine import _candidate
+    """Candidate lists of a packed shard into `out` at global ids `gids`
+    (bulk, in C: hostsrc/vsmat.c)."""
+    from . import _native as N
+    from .core import Candidate
 
-    tl, ll, sl = toks.tolist(), lens.tolist(), scores.tolist()
-    e = o = 0
-    for g, cnt in zip(np.asarray(gids).tolist(), count.tolist()):
-        per = []
-        for _ in range(cnt):
-            n_ = ll[e]
-            per.append(_candidate(tuple(tl[o:o + n_]), sl[e], g))
-            o += n_
-            e += 1
-        out[g] = per
+    mat = N.load_vsmat()
+    if len(toks):
+        mat.reserve(int(np.max(toks)) + 1)
+    mat.fill_packed(out, np.ascontiguousarray(np.asarray(gids), dtype=np.int64),
+                               np.ascontiguousarray(count, dtype=np.int32), np.ascontiguousarray(lens, dtype=np.int32),
+                               np.ascontiguousarray(scores, dtype=np.float64),
+                               np.ascontiguousarray(toks, dtype=np.int32), Candidate)
 
 
 def gather_packed(packed, group=None, dst: int = 0):

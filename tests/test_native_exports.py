@@ -117,3 +117,37 @@ def test_every_entry_rejects_bad_arguments_before_touching_the_device(lib):
     buf = C.create_string_buffer(64)
     p = C.addressof(buf)
     assert lib.vs_row_attention_grouped(p, 64, p, p, 0, 0, p, p, p, p, 1, p, 0, 16, 32, 0.125, None) == E
+
+
+def test_host_materialisation_extension_builds_candidates():
+    """_vsmat (hostsrc/vsmat.c) builds real Candidate objects in bulk: the
+    append layout (fill) and the packed gather layout (fill_packed)."""
+    import numpy as np
+
+    from paper_2010_02164_b200 import _native
+    from paper_2010_02164_b200.core import Candidate
+
+    mat = _native.load_vsmat()
+    k = 3
+    toks = np.array([9, 9, 0, 5, 2, 0, 7, 1, 2, 0, 4], dtype=np.int32)
+    count = np.array([2, 1], dtype=np.int32)
+    lens = np.array([3, 2, 0, 3, 0, 0], dtype=np.int32)
+    offs = np.array([2, 9, 0, 5, 0, 0], dtype=np.int32)
+    scores = np.array([-1.5, -2.25, 0, -0.125, 0, 0], dtype=np.float64)
+    out = [None] * 4
+    mat.fill(out, np.array([3, 1], dtype=np.int64), 0, count, lens, scores, offs, toks, k, Candidate)
+    assert out[3] == [Candidate((0, 5, 2), -1.5, True, 3), Candidate((0, 4), -2.25, True, 3)]
+    assert out[1] == [Candidate((0, 7, 1), -0.125, True, 1)]
+    c = out[3][0]
+    assert isinstance(c, Candidate) and hash(c) == hash(Candidate((0, 5, 2), -1.5, True, 3))
+    with pytest.raises(Exception):
+        c.score = 0.0  # frozen
+    out2 = [None] * 2
+    mat.fill_packed(out2, np.array([1, 0], dtype=np.int64), np.array([1, 2], dtype=np.int32),
+                    np.array([2, 1, 3], dtype=np.int32), np.array([-1.0, -2.0, -3.0]),
+                    np.array([0, 4, 0, 0, 6, 2], dtype=np.int32), Candidate)
+    assert out2[1] == [Candidate((0, 4), -1.0, True, 1)]
+    assert out2[0] == [Candidate((0,), -2.0, True, 0), Candidate((0, 6, 2), -3.0, True, 0)]
+    with pytest.raises(ValueError):
+        mat.fill(out, None, 0, count, lens, scores, np.array([2, 99, 0, 5, 0, 0], dtype=np.int32), toks, k,
+                 Candidate)
