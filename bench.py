@@ -367,7 +367,7 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batch
 LSTM_KW = dict(emb=128, hidden=256, max_src=128, seed=0, tau=4.0, eos_bias=3.0)
 
 
-def lstm_leg(reps: int = 2, batches: int = 2):
+def lstm_leg(reps: int = 2, batches: int = 4):
     """BASELINE.json configs[2]: the lightweight LSTM parsing shape (|V|=2,048,
     k=10, n=256, M=3, δ=10, N=20,000 synthetic) with its model — a 1-layer
     LSTM encoder-decoder with attention (decoder.LSTMScorer), the latency-bound

@@ -293,9 +293,16 @@ class GraphedTransformerScorer(TransformerScorer):
         for i, s_ in enumerate(srcs):
             pad[i, : len(s_)] = torch.from_numpy(s_.astype("int64"))
         cross = self.encode_sources(pad.to(engine.device), lens)
+        # K4, encoder half: each admitted source's cross-attention K/V rows into its slot
+        slots32 = slots.to(torch.int32)
+        es = self.enc_kv.element_size()
         for li, (ck, cv) in enumerate(cross):
-            self.enc_kv[li, 0, slots, :S] = ck
-            self.enc_kv[li, 1, slots, :S] = cv
+            for plane, src in ((0, ck), (1, cv)):
+                src = src.contiguous()
+                dst = self.enc_kv[li, plane]
+                N.check(engine.lib.vs_scatter_rows(dst.data_ptr(), dst.stride(0) * es, src.data_ptr(),
+                                                   src.stride(0) * es, S * self.d * es, slots32.data_ptr(),
+                                                   None, na, engine.stream_ptr), "vs_scatter_rows")
         self.enc_len[slots] = lens.to(torch.int32)
 
     def _row_attn(self, q, kc, vc, idx, lens, knew, vnew, out):
