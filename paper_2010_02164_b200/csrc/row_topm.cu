@@ -500,7 +500,40 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   auto boot = [&](float lm, int lt) {
     float m0;
     if constexpr (TL) {
-      m0 = tl_seed(tl, lm, lt, Meff, lane);
+      if (W > 1) {
+        // the W parts of a row pool their 32 lane maxima: every part starts with
+        // θ = the Meff-th largest of the W·32 (a bound with token "+inf", so every
+        // element of that value passes) and an empty list.  The Meff largest maxima
+        // are distinct elements >= θ, each inserted by its own part, so the merged
+        // top-Meff is exact and the proof holds; a W-times larger window gives a
+        // higher θ and fewer insertions per part.
+        // the row's parts' candidate buffers (contiguous, unused until the epilogue)
+        uint64_t* pool = sbuf[wid - part];
+        pool[part * 32 + lane] = lm == -INFINITY ? 0ull : (uint64_t)KeyOps<K>::key(lm, lt);
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");
+        uint64_t v[WPC];
+#pragma unroll
+        for (int q = 0; q < WPC; ++q) v[q] = q < W ? pool[q * 32 + lane] : 0ull;
+        uint64_t kth = 0, prev = ~0ull;
+        for (int j = 0; j < Meff; ++j) {  // Meff rounds: largest key strictly below prev
+          uint64_t b = 0;
+#pragma unroll
+          for (int q = 0; q < WPC; ++q) b = (v[q] < prev && v[q] > b) ? v[q] : b;
+          b = warp_max_u64(b);
+          kth = prev = b;
+          if (b == 0) break;
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");  // pool read by all
+        tl.tk = (K)0;
+        if (kth != 0) {
+          const float t0 = KeyOps<K>::val((K)kth);
+          tl.theta = KeyOps<K>::bound(t0);
+          tl.theta_x = t0;
+        }
+        m0 = 0.0f;
+      } else {
+        m0 = tl_seed(tl, lm, lt, Meff, lane);
+      }
     } else {
 #pragma unroll
       for (int k = 2; k <= 32; k <<= 1)

@@ -891,3 +891,25 @@ def test_lstm_scorer_decisions_match_oracle_replay_and_eager():
     assert [[(c.tokens, c.score) for c in per] for per in out] == O.signature(want)
     *_, out2, rep2 = _lstm_run(use_graphs=False)
     assert [[(c.tokens, c.score) for c in per] for per in out2] == [[(c.tokens, c.score) for c in per] for per in out]
+
+
+@pytest.mark.parametrize("M", [1, 5, 8, 32])
+def test_row_topm_split_rows_with_concentrated_and_tied_maxima(M):
+    """Small steps run several warps per row whose bootstrap θ is pooled across
+    the row's parts: rows whose largest values all sit in one part, rows made of
+    ties, and a row whose maximum is in the scalar tail stay exact (warp kernel
+    and split kernel)."""
+    P, *_ = _pkg()
+    V = 42023  # odd: a scalar tail
+    rng = np.random.default_rng(17)
+    x = rng.normal(0, 1, (4, V)).astype(np.float32)
+    x[0, 40000:40040] += 9.0          # the top region inside the last part
+    x[1, :] = 0.5                       # all tied
+    x[1, 7::997] = 0.75
+    x[2, V - 1] = 50.0                  # maximum in the tail
+    x[3, :] = np.round(x[3, :], 1)     # heavy ties
+    for dt in (torch.float32, torch.bfloat16):
+        dx = torch.from_numpy(x).cuda().to(dt)
+        for kernel in ("warp", "split"):
+            tok, lp, lse, _ = P.row_lse_topm(dx, M, kernel=kernel)
+            _check_rows(dx.float().cpu().numpy(), M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
