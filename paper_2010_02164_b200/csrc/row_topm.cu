@@ -761,7 +761,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
   // ---- lse: in-order left fold of the row's segment pairs ----------------------------
   // lane q holds pair q; the max and the rescaled sum are fixed xor trees over
   // the same NSEG+1 pairs in every warp of the row (partition-invariant)
-  if (W > 1) __syncthreads();
+  // the W warps of this row only (named barrier 1 + row-in-CTA): a row never
+  // waits for the other rows of its CTA
+  if (W > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");
   else __syncwarp();
   float s;
   {
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
       spart[wid].theta_x = c.theta_x;
       spart[wid].cnt = c.cnt;
     }
-    __syncthreads();
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");
     if (part != 0 || !active) return;
     // leader: gather the other parts' candidates behind its own (CAPW suffices:
     // each part holds < flush_at + 256 entries only transiently; after the
