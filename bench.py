@@ -388,6 +388,66 @@ def lstm_leg(reps: int = 2, batches: int = 4):
             "driver": "synchronous (status read per step), decoder step = 1 CUDA-graph replay per row bucket"}
 
 
+def _lstm_cpu_worker(args):
+    """Spawned process: the reference search (oracle beam_decode, bb/search.py:233-242)
+    with the CPU mirror of the LSTM model (oracle/scorers.py:LSTMDecoderCPU,
+    stateless prefix recompute, fp64 rows) on a few inputs; returns per-input
+    outputs and the busy time."""
+    w, items = args
+    import torch
+
+    torch.set_num_threads(1)
+    from oracle import varstream_oracle as O
+    from oracle.scorers import LSTMDecoderCPU
+
+    kw = {k: v for k, v in LSTM_KW.items() if k != "max_src"}
+    sc = LSTMDecoderCPU(w["V"], w["sos"], w["eos"], **kw)
+    cfg = O.OConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                    max_len=w["max_len"])
+    t0 = time.perf_counter()
+    out = [(q, [(c.tokens, c.score) for c in O.beam_decode(sc.encode(toks, q), sc, cfg)]) for q, toks in items]
+    return time.perf_counter() - t0, out
+
+
+def lstm_reference(w, n_inputs: int = 64, procs: int | None = None):
+    """configs[2]'s CPU baseline and agreement: the reference search driving
+    the same random-init LSTM weights on the host cores (one process per core,
+    an evenly strided sample), and the device decode of the same inputs compared
+    with it (identical lists / top-1; bf16 device operands vs fp32 CPU)."""
+    import multiprocessing as mp
+
+    from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
+    from paper_2010_02164_b200.decoder import LSTMScorer
+    from oracle.agreement import compare
+
+    corpus = _corpus(w)
+    stride = max(1, len(corpus) // n_inputs)
+    sample = corpus[stride // 2::stride][:n_inputs]
+    procs = procs or min(len(sample), os.cpu_count() or 1, 64)
+    chunks = [[(q, sample[q]) for q in range(p, len(sample), procs)] for p in range(procs)]
+    with mp.get_context("spawn").Pool(procs) as pool:
+        res = pool.map(_lstm_cpu_worker, [(w, c) for c in chunks])
+    busy = max(r[0] for r in res)
+    cpu = dict(x for r in res for x in r[1])
+    vocab = Vocabulary(w["V"], w["sos"], w["eos"])
+    cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
+                       max_len=w["max_len"])
+    gpu, _ = run_varstream(sample, LSTMScorer(vocab, **LSTM_KW), cfg)
+    same = top1 = 0
+    for q in range(len(sample)):
+        s_, t_ = compare([(c.tokens, c.score) for c in gpu[q]], cpu[q])
+        same += s_
+        top1 += t_
+    n = len(sample)
+    return ({"value": round(n / busy, 3), "unit": "seq/s", "cores": procs, "kind": "port",
+             "sample": f"{n} of {len(corpus)} inputs (every {stride}th of the length-sorted corpus), {procs} "
+                       f"processes x 1 thread, the reference search + CPU LSTM (stateless prefix recompute, "
+                       f"fp64 rows), slowest {busy:.1f}s"},
+            {"inputs": n, "identical_fraction": round(same / n, 4), "top1_fraction": round(top1 / n, 4),
+             "reference": "oracle beam_decode + LSTMDecoderCPU (same random-init weights, bf16-rounded operands, "
+                          "fp32 compute, fp64 log-softmax rows)"})
+
+
 def toy_model_engines(reps: int = 2):
     """BASELINE.json configs[0]/[1] with a small random-init decoder: Fixed vs
     VarBeam vs FixedStream vs VarStream (ε sweep) on the toy workload
@@ -792,6 +852,10 @@ def run_ours(args):
         if args.model_legs:
             line["engines_toy_c2_model"] = toy_model_engines()
             line["lstm_parse_c3"] = lstm_leg()
+            if not args.no_cpu_baseline:
+                cpu_l, agree_l = lstm_reference(WORKLOADS["parse_c3"])
+                line["lstm_parse_c3"]["cpu_baseline"] = cpu_l
+                line["lstm_parse_c3"]["reference_agreement"] = agree_l
     if rank == 0 and world == 1 and args.decoder_inputs > 0:
         line["decoder_wmt19"] = decoder_leg(w, args.decoder_inputs, batches=3)
         line["decoder_wmt19_k5"] = decoder_leg(w, args.decoder_inputs, fused_head=True, batches=3)

@@ -77,6 +77,27 @@ def test_cli_device_run_writes_results_and_trace(tmp_path):
     doc = ResultsDocument.read(out)
     assert len(doc.records) == 40 and all(1 <= len(r["candidates"]) <= 5 for r in doc.records)
     assert (tmp_path / "r.json.trace.csv").read_text().startswith("timestep,expansions")
+    # against the reference algorithm (oracle, pinned to bb/*) computing its own fp64
+    # log-softmax rows of the same logits, in the reference's experiment order
+    # (synthesise, bucket, decode, restore input order: bb/harness.py:280-331)
+    import math
+
+    from oracle import varstream_oracle as O
+    from oracle.scorers import HashLogitsCPU
+
+    corpus = O.generate_synthetic_corpus(0, 40, 1000, mean_len=6.0)
+    bucketed, perm = O.bucket_by_length(corpus)
+    sc = HashLogitsCPU(1000, 0, 2, 3, scale=0.5, power=0, eos_bias=4.0, dtype="bf16")
+    cfg = O.OConfig(k=5, n=8, delta=1.5, max_candidates=3, max_len=30)
+    want, wrep = O.run_varstream(bucketed, sc, cfg)
+    same = 0
+    for pos, orig in enumerate(perm):
+        got = [(tuple(c["tokens"]), c["score"]) for c in doc.records[orig]["candidates"]]
+        ref = [(c.tokens, c.score) for c in want[pos]]
+        same += len(got) == len(ref) and all(
+            a[0] == b[0] and math.isclose(a[1], b[1], rel_tol=1e-5) for a, b in zip(got, ref))
+    assert same >= 0.995 * 40, same
+    assert doc.metrics["candidate_expansions"] == wrep.candidate_expansions
 
 
 def test_experiment_config_validation_matches_reference():
