@@ -262,6 +262,12 @@ int vs_scatter_rows(void* dst, int64_t dst_stride_bytes, const void* src, int64_
                     int64_t bytes, const int32_t* slots, const int32_t* d_count, int32_t count_max,
                     void* stream);
 
+/* Row LayerNorm without affine for bf16 activations (the decoder scorers):
+ * y[r] = (x[r] - mean) * rsqrt(var + eps), fp32 statistics, bf16 out; warp per
+ * row; d a multiple of 256 up to 4096, 16-byte aligned rows. */
+int vs_layer_norm_bf16(const void* x, int64_t ldx, void* y, int64_t ldy, int32_t R, int32_t d, float eps,
+                       void* stream);
+
 /* Synthetic device scorer (stands in for the decoder's logits; mirrors the
  * structure of bb/model.py:209-218 SeededHashScorer with an integer hash).
  * vs_hash_encode: per admitted slot (status admitted list) computes the

@@ -65,7 +65,7 @@ class VsHashParams(C.Structure):
 EXPORTS = ("vs_version", "vs_row_lse_topm", "vs_row_lse_topm_ws", "vs_row_lse_topm_ws_bytes", "vs_beam_step",
            "vs_beam_step_schedule", "vs_schedule", "vs_schedule_mirror", "vs_rows_copy",
            "vs_scatter_rows", "vs_hash_encode", "vs_hash_logits", "vs_row_attention", "vs_row_attention_grouped",
-           "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes", "vs_row_topm_f64")
+           "vs_proj_lse_topm", "vs_proj_lse_topm_ws_bytes", "vs_row_topm_f64", "vs_layer_norm_bf16")
 
 _lib = None
 
@@ -87,6 +87,7 @@ def load_library(path: Path | None = None) -> C.CDLL:
                                i32),
         "vs_row_lse_topm_ws_bytes": ([i32, i32, i32], C.c_size_t),
         "vs_row_topm_f64": ([vp, i64, i32, i32, i32, vp, i32, vp, vp, vp, vp], i32),
+        "vs_layer_norm_bf16": ([vp, i64, vp, i64, i32, i32, C.c_float, vp], i32),
         "vs_beam_step": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, vp], i32),
         "vs_schedule": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp], i32),
         "vs_schedule_mirror": ([C.POINTER(VsConfig), C.POINTER(VsState), i32, i32, i32, i32, i32, vp, vp], i32),

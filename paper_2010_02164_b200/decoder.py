@@ -305,6 +305,14 @@ class GraphedTransformerScorer(TransformerScorer):
                                                    None, na, engine.stream_ptr), "vs_scatter_rows")
         self.enc_len[slots] = lens.to(torch.int32)
 
+    def _ln(self, x):
+        """LayerNorm of the [rows, d] bf16 activations (vs_layer_norm_bf16)."""
+        y = torch.empty_like(x)
+        N.check(self.engine.lib.vs_layer_norm_bf16(x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0), x.shape[0],
+                                                   self.d, 1e-5, torch.cuda.current_stream(self.device).cuda_stream),
+                "vs_layer_norm_bf16")
+        return y
+
     def _row_attn(self, q, kc, vc, idx, lens, knew, vnew, out):
         lib = self.engine.lib
         R = q.shape[0]
@@ -345,11 +353,11 @@ class GraphedTransformerScorer(TransformerScorer):
             self._row_attn(qkv[:, :d], self.kv[li, 0], self.kv[li, 1], phys_kv, ln, qkv[:, d:2 * d],
                        qkv[:, 2 * d:], att)
             # residual adds in the GEMM epilogue (addmm: one rounding, no separate add kernel)
-            x = F.layer_norm(torch.addmm(x, att, L["o"].T), (d,))
+            x = self._ln(torch.addmm(x, att, L["o"].T))
             cq = x @ L["cq"].T
             self._row_attn_grouped(cq, self.enc_kv[li, 0], self.enc_kv[li, 1], slot, enc_len, att)
-            x = F.layer_norm(torch.addmm(x, att, L["co"].T), (d,))
-            x = F.layer_norm(torch.addmm(x, F.gelu(x @ L["f1"].T), L["f2"].T), (d,))
+            x = self._ln(torch.addmm(x, att, L["co"].T))
+            x = self._ln(torch.addmm(x, F.gelu(x @ L["f1"].T), L["f2"].T))
         lg = self.lg[:Rb, : self.vocab.size]
         eos = self.vocab.eos
         src_len = t["slot_src_len"][slot.long()].float()

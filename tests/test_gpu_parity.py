@@ -913,3 +913,20 @@ def test_row_topm_split_rows_with_concentrated_and_tied_maxima(M):
         for kernel in ("warp", "split"):
             tok, lp, lse, _ = P.row_lse_topm(dx, M, kernel=kernel)
             _check_rows(dx.float().cpu().numpy(), M, tok.cpu().numpy(), lp.cpu().numpy(), lse.cpu().numpy())
+
+
+@pytest.mark.parametrize("d", [256, 1024])
+def test_layer_norm_kernel_matches_torch(d):
+    """vs_layer_norm_bf16 (decoder LayerNorm) vs F.layer_norm on bf16 rows:
+    within one bf16 ulp of the fp32 result."""
+    P, N, *_ = _pkg()
+    lib = N.load_library()
+    g = torch.Generator(device="cuda").manual_seed(d)
+    x = (torch.randn((333, d), generator=g, device="cuda") * 3 + 1.5).to(torch.bfloat16)
+    y = torch.empty_like(x)
+    N.check(lib.vs_layer_norm_bf16(x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0), x.shape[0], d, 1e-5,
+                                   torch.cuda.current_stream().cuda_stream), "ln")
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.layer_norm(x.float(), (d,))
+    assert torch.allclose(y.float(), ref, rtol=1e-2, atol=1e-2)
+    assert (y.float() - torch.nn.functional.layer_norm(x, (d,)).float()).abs().max() <= 0.02
