@@ -511,22 +511,29 @@ __global__ void __launch_bounds__(WPC * 32, MINB) row_lse_topm_warp_kernel(
         uint64_t* pool = sbuf[wid - part];
         pool[part * 32 + lane] = lm == -INFINITY ? 0ull : (uint64_t)KeyOps<K>::key(lm, lt);
         asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");
-        uint64_t v[WPC];
-#pragma unroll
-        for (int q = 0; q < WPC; ++q) v[q] = q < W ? pool[q * 32 + lane] : 0ull;
-        uint64_t kth = 0, prev = ~0ull;
+        K kth = 0, prev = (K)~(K)0;
         for (int j = 0; j < Meff; ++j) {  // Meff rounds: largest key strictly below prev
-          uint64_t b = 0;
+          K b = 0;
+          for (int q = 0; q < W; ++q) {
+            const K vq = (K)pool[q * 32 + lane];
+            b = (vq < prev && vq > b) ? vq : b;
+          }
+          if constexpr (sizeof(K) == 4) {
 #pragma unroll
-          for (int q = 0; q < WPC; ++q) b = (v[q] < prev && v[q] > b) ? v[q] : b;
-          b = warp_max_u64(b);
+            for (int o = 16; o > 0; o >>= 1) {
+              const K ob = (K)__shfl_xor_sync(FULL, (uint32_t)b, o);
+              b = ob > b ? ob : b;
+            }
+          } else {
+            b = (K)warp_max_u64((uint64_t)b);
+          }
           kth = prev = b;
           if (b == 0) break;
         }
         asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / W), "r"(W * 32) : "memory");  // pool read by all
         tl.tk = (K)0;
         if (kth != 0) {
-          const float t0 = KeyOps<K>::val((K)kth);
+          const float t0 = KeyOps<K>::val(kth);
           tl.theta = KeyOps<K>::bound(t0);
           tl.theta_x = t0;
         }
