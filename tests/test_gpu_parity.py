@@ -930,3 +930,49 @@ def test_layer_norm_kernel_matches_torch(d):
     ref = torch.nn.functional.layer_norm(x.float(), (d,))
     assert torch.allclose(y.float(), ref, rtol=1e-2, atol=1e-2)
     assert (y.float() - torch.nn.functional.layer_norm(x, (d,)).float()).abs().max() <= 0.02
+
+
+def _nccl_worker(rank, world, port, out_path):
+    import os
+    import pickle
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda:0"))
+    import paper_2010_02164_b200 as P
+    from paper_2010_02164_b200.parallel import run_varstream_sharded
+    from paper_2010_02164_b200.scorers import DeviceHashScorer
+
+    vocab = P.Vocabulary(3000, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=12, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=30)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(9, 150, 3000, mean_len=8.0, clip=25))
+    sc = DeviceHashScorer(vocab, 29, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    res, _ = run_varstream_sharded(corpus, sc, cfg, streams=2)
+    with open(out_path, "wb") as f:
+        pickle.dump([[(c.tokens, c.score) for c in per] for per in res], f)
+    dist.destroy_process_group()
+
+
+def test_nccl_gather_path_single_rank(tmp_path):
+    """The multi-GPU data plane over NCCL (one rank on this GPU: the all-reduce
+    of the message size and the gather of the packed message run through
+    ProcessGroupNCCL) returns the single-process outputs."""
+    import pickle
+    import socket
+
+    import torch.multiprocessing as mp
+
+    P, N, SearchEngine, DeviceHashScorer, _, _ = _pkg()
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    out = tmp_path / "nccl.pkl"
+    mp.spawn(_nccl_worker, args=(1, port, str(out)), nprocs=1, join=True)
+    vocab = P.Vocabulary(3000, 0, 2)
+    cfg = P.DecodeConfig(k=6, n=12, epsilon=1 / 6, delta=1.5, max_candidates=3, max_len=30)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(9, 150, 3000, mean_len=8.0, clip=25))
+    sc = DeviceHashScorer(vocab, 29, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
+    want, _ = P.run_varstream(corpus, sc, cfg)
+    assert pickle.loads(out.read_bytes()) == [[(c.tokens, c.score) for c in per] for per in want]
