@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import os
 import math
 from dataclasses import dataclass
 from typing import Callable
@@ -428,7 +429,7 @@ class SearchEngine:
 
     def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 16,
                     trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None,
-                    steps_per_graph: int = 4, harvest_into: list | None = None, gids=None):
+                    steps_per_graph: int | None = None, harvest_into: list | None = None, gids=None):
         """Generator form of the host-sync-free driver: every ``next()``
         launches a few steps (on the CUDA stream current at that call) and
         consumes status snapshots ``ring`` steps behind; it returns the
@@ -453,6 +454,8 @@ class SearchEngine:
         report = MetricsReport.new(trace=trace)
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
         graphed = getattr(scorer, "graph_safe", False) and k1_events is None
+        if steps_per_graph is None:
+            steps_per_graph = int(os.environ.get("VS_STEPS_PER_GRAPH", "8"))
         spg = max(1, steps_per_graph) if graphed else 1
         ring = max(ring, 2 * spg)
         ring += (-ring) % spg  # a multiple of spg: graph g always writes the same slots
