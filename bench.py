@@ -349,7 +349,14 @@ def decoder_leg(w, n_inputs: int, reps: int = 2, fused_head: bool = False, batch
     sample = corpus[::stride][:n_inputs]
     t, rep, dec = _model_leg(w, sample, lambda v: GraphedTransformerScorer(
         v, tau=DEC_TAU, eos_bias=DEC_EOS_BIAS, max_src=256, seed=0, fused_head=fused_head), batches, reps)
+    k5 = None
+    kf = ROOT / "profiles" / "round2" / "k5_1424_ncu.json"
+    if fused_head and kf.exists():
+        kj = json.loads(kf.read_text())
+        k5 = {"tensor_pipe_active_pct": kj["tensor_pipe_active_pct"], "R": kj["R"],
+              "dram_write_bytes_per_launch": kj["dram_write_bytes"], "source": "profiles/round2/k5_1424_ncu.json"}
     return {"value": round(len(sample) / t, 2), "unit": "seq/s", "inputs": len(sample),
+            "k5_profile": k5,
             "sample": "the whole corpus" if stride == 1 else
                       f"every {stride}th input of the {len(corpus)}-input length-sorted corpus",
             "ms_per_decode": round(1e3 * t, 2), "timesteps": rep.timesteps,
