@@ -623,6 +623,20 @@ def decoder_cpu_baseline(w, procs: int = 8):
                       f"candidate expansions (whole-prefix recompute per candidate, fp32), slowest {busy:.1f}s"}
 
 
+def bench_config(args, w, n_total: int, world: int) -> dict:
+    """The workload description both arms print (the driver compares them)."""
+    S = max(1, args.streams)
+    return {"workload": f"{args.workload}: |V|={w['V']} k={w['k']} n={w['n']} M={w['M']} "
+                        f"delta={w['delta']} eps=1/6 max_len={w['max_len']} N={n_total}",
+            "scorer": f"device hash scorer (log-like logits, scale {w['scale']}, eos_bias {w['eos_bias']}) "
+                      "standing in for the decoder vocab projection (CPU mirror on the reference arm)",
+            "global_batch": n_total, "batch_slots_n": w["n"], "parallelism": f"shard{world}",
+            "scaling": args.scaling, "concurrent_batches_per_gpu": S,
+            "l2": "inputs larger than L2 (~130 GB of logits stream through K1 per decode, L2 126 MB); not "
+                  "flushed between the decode's own kernels (producer -> K1 reuse is part of the pipeline); "
+                  "roofline.full_width flushes L2 (256 MB write) before each 538 MB launch"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -808,23 +822,10 @@ def run_ours(args):
         "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "bf16 logits / fp32 lse / fp64 scores",
         "data": "synthetic (reference generator bb/harness.py:85-115, seed %d; device hash scorer)" % w["seed"],
-        "config": {"workload": f"{args.workload}: |V|={w['V']} k={w['k']} n={w['n']} M={w['M']} "
-                               f"delta={w['delta']} eps=1/6 max_len={w['max_len']} N={len(corpus)}",
-                   "scorer": f"device hash scorer (log-like logits, scale {w['scale']}, eos_bias "
-                             f"{w['eos_bias']}) standing in for the decoder vocab projection",
-                   "global_batch": len(corpus), "batch_slots_n": w["n"], "parallelism": f"shard{world}",
-                   "concurrent_batches_per_gpu": S,
-                   "concurrency": f"{S} independent refilling batches of n={w['n']} slots per GPU on separate "
-                                  "CUDA streams (the corpus dealt snake-wise over them, as across GPUs); "
-                                  "outputs identical to one batch (tested)",
-                   "l2": "inputs larger than L2: one bench step streams "
-                         f"{rep.candidate_expansions * w['V'] * 2 / 1e9:.1f} GB of logits through K1 "
-                         "(L2 126 MB); not flushed between the decode's own kernels (producer -> K1 "
-                         "reuse is part of the pipeline); roofline_full_width flushes L2 (256 MB write) "
-                         "before each 538 MB launch",
-                   "timesteps_per_decode": rep.timesteps,
-                   "expansions_per_decode": rep.candidate_expansions,
-                   "expansions_per_step": round(rep.expansions_per_step, 1)},
+        "config": bench_config(args, w, len(corpus), world),
+        "decode": {"timesteps_per_decode": rep.timesteps, "expansions_per_decode": rep.candidate_expansions,
+                   "expansions_per_step": round(rep.expansions_per_step, 1),
+                   "logits_gb_per_decode": round(rep.candidate_expansions * w["V"] * 2 / 1e9, 1)},
         "roofline": {"kernel": "vs_row_lse_topm (K1), in-decode", "bound": "hbm",
                      "regime": "L2-resident and latency-bound: the scorer writes each step's logits "
                                "(~" f"{k1_bytes / max(1, len(k1)) / 1e6:.0f}" " MB) into the 126 MB L2 and K1 reads "
@@ -891,7 +892,9 @@ def run_reference(args):
     w = WORKLOADS[args.workload]
     if args.n_inputs:
         w = dict(w, N=args.n_inputs)
-    corpus = _corpus(w)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n_total = args.strong_n if args.scaling == "strong" else w["N"] * world  # the same corpus as our arm
+    corpus = _corpus(dict(w, N=n_total))
     vals = []
     for i in range(args.warmup + args.steps):
         v, cores, txt, _, _ = cpu_reference(w, corpus, per_proc=args.cpu_per_proc)
@@ -903,7 +906,7 @@ def run_reference(args):
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
         "warmup": args.warmup, "higher_is_better": True, "vs_baseline": None,
         "dtype": "fp64 rows / fp64 scores", "data": "synthetic",
-        "config": {"workload": args.workload, "global_batch": w["N"]},
+        "config": bench_config(args, w, len(corpus), world),
         "cpu_baseline": {"value": round(value, 3), "unit": "seq/s", "cores": cores, "kind": "port",
                          "sample": txt},
         "e2e": {"value": round(value, 3), "unit": "seq/s", "h2d_bytes_per_step": 0,
