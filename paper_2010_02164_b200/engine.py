@@ -429,7 +429,8 @@ class SearchEngine:
 
     def async_steps(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int, ring: int = 16,
                     trace: bool = False, src_tok=None, src_off=None, k1_events: list | None = None,
-                    steps_per_graph: int | None = None, harvest_into: list | None = None, gids=None):
+                    steps_per_graph: int | None = None, harvest_into: list | None = None, gids=None,
+                    harvest_chunk: int = 256):
         """Generator form of the host-sync-free driver: every ``next()``
         launches a few steps (on the CUDA stream current at that call) and
         consumes status snapshots ``ring`` steps behind; it returns the
@@ -462,7 +463,7 @@ class SearchEngine:
         if self._hdr is None or self._hdr.shape[0] != ring:
             self._hdr = torch.zeros((ring, N.ST_HDR), dtype=torch.int32, pin_memory=True)
         hdr = self._hdr
-        harvest = Harvest(self, harvest_into, gids) if harvest_into is not None else None
+        harvest = Harvest(self, harvest_into, gids, harvest_chunk) if harvest_into is not None else None
         events = [torch.cuda.Event() for _ in range(ring)]
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)

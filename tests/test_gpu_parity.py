@@ -976,3 +976,26 @@ def test_nccl_gather_path_single_rank(tmp_path):
     sc = DeviceHashScorer(vocab, 29, scale=0.5, power=0, eos_bias=5.0, dtype="bf16")
     want, _ = P.run_varstream(corpus, sc, cfg)
     assert pickle.loads(out.read_bytes()) == [[(c.tokens, c.score) for c in per] for per in want]
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 10 ** 9])
+def test_streamed_output_harvest_matches_synchronous_results(chunk):
+    """Harvest: outputs copied and materialised while the device decodes
+    (chunks of finished inputs below MINLIVE, appended token ranges below
+    TOKFILL) equal the synchronous driver's results for any chunk size."""
+    P, N, SearchEngine, DeviceHashScorer, _, _ = _pkg()
+    vocab = P.Vocabulary(2000, 0, 2)
+    cfg = P.DecodeConfig(k=7, n=10, epsilon=1 / 5, delta=1.5, max_candidates=3, max_len=28)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(12, 130, 2000, mean_len=7.0, clip=20))
+    sc = DeviceHashScorer(vocab, 41, scale=0.5, power=0, eos_bias=4.0, dtype="bf16")
+    want, wrep = SearchEngine(cfg, vocab).run(corpus, sc, admit_mode=N.VS_ADMIT_VARSTREAM,
+                                              select_mode=N.VS_SELECT_MIN_LT, flush_enabled=False)
+    eng = SearchEngine(cfg, vocab)
+    out = [[] for _ in range(len(corpus))]
+    gen = eng.async_steps(corpus, sc, admit_mode=N.VS_ADMIT_VARSTREAM, select_mode=N.VS_SELECT_MIN_LT,
+                          harvest_into=out, harvest_chunk=chunk)
+    for _ in gen:
+        pass
+    assert [[(c.tokens, c.score, c.input_id) for c in per] for per in out] == \
+        [[(c.tokens, c.score, c.input_id) for c in per] for per in want]
+    assert eng.last_d2h_bytes > 0
