@@ -454,10 +454,12 @@ class SearchEngine:
         scorer.bind(self)
         report = MetricsReport.new(trace=trace)
         cost = CostParams(cfgd.cost_c0, cfgd.cost_c1)
-        graphed = getattr(scorer, "graph_safe", False) and k1_events is None
+        graphed = getattr(scorer, "graph_safe", False)
         if steps_per_graph is None:
             steps_per_graph = int(os.environ.get("VS_STEPS_PER_GRAPH", "8"))
-        spg = max(1, steps_per_graph) if graphed else 1
+        # K1 timing (k1_events): one step per graph, timing events captured around
+        # K1 as graph nodes, read back as each step's snapshot is consumed
+        spg = max(1, steps_per_graph) if graphed and k1_events is None else 1
         ring = max(ring, 2 * spg)
         ring += (-ring) % spg  # a multiple of spg: graph g always writes the same slots
         if self._hdr is None or self._hdr.shape[0] != ring:
@@ -468,7 +470,8 @@ class SearchEngine:
         cap = self.capacity
         d_R = self.status_ptr(N.ST_R)
         launched = processed = 0
-        graphs = self._step_graphs(scorer, ring, spg, admit_mode, select_mode) if graphed else None
+        graphs = self._step_graphs(scorer, ring, spg, admit_mode, select_mode,
+                                   k1_timing=k1_events is not None) if graphed else None
         stream = torch.cuda.current_stream(self.device)
         self.schedule(first=True, remove=False, admit=admit_mode, select=select_mode, mirror=hdr[0].data_ptr())
         events[0].record(stream)
@@ -478,6 +481,9 @@ class SearchEngine:
             # up to launched+spg: everything older than that must be consumed
             while launched + spg - processed >= ring:
                 events[processed % ring].synchronize()
+                if graphs is not None and k1_events is not None and processed >= 1:
+                    e0, e1 = self._graph_events[(processed - 1) % len(graphs)]
+                    k1_events.append(e0.elapsed_time(e1))  # step processed-1 has completed
                 st = hdr[processed % ring].numpy()
                 if st[N.ST_ERROR]:
                     self.read_status()
@@ -504,7 +510,8 @@ class SearchEngine:
                     self.row_topm(logits, code, 0, cap, d_R)
                 if k1_events is not None:
                     e1.record(stream)
-                    k1_events.append((e0, e1))
+                    e1.synchronize()
+                    k1_events.append(e0.elapsed_time(e1))
                 self.beam_step_schedule(admit=admit_mode, select=select_mode,
                                         mirror=hdr[(launched + 1) % ring].data_ptr())
                 scorer.after_step(self, None)
@@ -522,16 +529,18 @@ class SearchEngine:
             self.last_d2h_bytes = harvest.d2h_bytes
         return report
 
-    def _step_graphs(self, scorer, ring: int, spg: int, admit_mode: int, select_mode: int):
+    def _step_graphs(self, scorer, ring: int, spg: int, admit_mode: int, select_mode: int,
+                     k1_timing: bool = False):
         """Capture (once per engine state / scorer binding) ring/spg graphs of
         spg steps each: scorer launches, K1, K2+K3 (status header -> the next
-        pinned slot)."""
+        pinned slot).  k1_timing: external timing events around each K1 as
+        graph nodes (spg = 1), so K1 is timed on the device with no host gaps."""
         # the graphs bake in the scorer's parameters and buffer addresses: key on
         # the scorer object itself (held strongly, compared with `is`, so a
         # recycled id() can never match) plus its graph_key() (parameters and
         # data pointers, which change when bind() reallocates)
         gk = scorer.graph_key() if hasattr(scorer, "graph_key") else None
-        key = (gk, ring, spg, admit_mode, select_mode, self.N,  # N is a K3 launch argument
+        key = (gk, ring, spg, admit_mode, select_mode, k1_timing, self.N,  # N is a K3 launch argument
                tuple(getattr(self.state, f) for f in N.STATE_FIELDS), self._hdr.data_ptr())
         if self._graph_key == key and self._graph_scorer is scorer:
             return self._graphs
@@ -540,21 +549,29 @@ class SearchEngine:
         if self._k1_ws is None or self._k1_ws.numel() < nbytes:  # allocate outside the capture
             self._k1_ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         torch.cuda.current_stream(self.device).synchronize()
-        graphs = []
+        graphs, gev = [], []
         for gi in range(ring // spg):
             g = torch.cuda.CUDAGraph()
+            if k1_timing:
+                gev.append((torch.cuda.Event(enable_timing=True, external=True),
+                            torch.cuda.Event(enable_timing=True, external=True)))
             with torch.cuda.graph(g):
                 for q in range(spg):
                     step = gi * spg + q
                     scorer.on_admit(self, None)
                     logits, code = scorer.logits(self, None)
+                    if k1_timing:
+                        gev[-1][0].record()
                     if code != N.VS_K1_DONE:
                         self.row_topm(logits, code, 0, cap, d_R)
+                    if k1_timing:
+                        gev[-1][1].record()
                     self.beam_step_schedule(admit=admit_mode, select=select_mode,
                                             mirror=self._hdr[(step + 1) % ring].data_ptr())
                     scorer.after_step(self, None)
             graphs.append(g)
         self._graphs, self._graph_key, self._graph_scorer = graphs, key, scorer
+        self._graph_events = gev
         return graphs
 
     def run_async(self, corpus=None, scorer=None, *, admit_mode: int, select_mode: int,
