@@ -100,22 +100,28 @@ class Harvest:
             self._request(hi, int(st[N.ST_TOKFILL]))
         self.poll()
 
-    def _request(self, hi: int, fill: int) -> None:
+    def _request(self, hi: int, fill: int, compact: bool = False) -> None:
         t, k, lo = self.eng.t, self.eng.k, self.lo
-        src = (t["out_count"][lo:hi], t["out_len"][lo * k:hi * k], t["out_score"][lo * k:hi * k],
-               t["out_off"][lo * k:hi * k], t["out_tok"][self.tok_hi:fill])
+        if compact:  # only the emitted candidates' metadata (a device sync: used once the run is over)
+            cnt = t["out_count"][lo:hi]
+            emitted = (torch.arange(k, device=cnt.device)[None, :] < cnt[:, None]).reshape(-1)
+            src = (cnt, t["out_len"][lo * k:hi * k][emitted], t["out_score"][lo * k:hi * k][emitted],
+                   t["out_off"][lo * k:hi * k][emitted], t["out_tok"][self.tok_hi:fill])
+        else:
+            src = (t["out_count"][lo:hi], t["out_len"][lo * k:hi * k], t["out_score"][lo * k:hi * k],
+                   t["out_off"][lo * k:hi * k], t["out_tok"][self.tok_hi:fill])
         host = tuple(torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in src)
         for h, x in zip(host, src):
             h.copy_(x, non_blocking=True)
             self.d2h_bytes += h.numel() * h.element_size()
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.eng.device))
-        self.pending.append((ev, lo, hi, host))
+        self.pending.append((ev, lo, hi, host, 0 if compact else k))
         self.lo, self.tok_hi = hi, fill
 
     def poll(self, block: bool = False) -> None:
         while self.pending and (block or self.pending[0][0].query()):
-            ev, lo, hi, host = self.pending.pop(0)
+            ev, lo, hi, host, stride = self.pending.pop(0)
             ev.synchronize()
             count, lens, scores, offs, tok = (h.numpy() for h in host)
             end = self.landed + tok.shape[0]
@@ -126,14 +132,14 @@ class Harvest:
             self.toks[self.landed:end] = tok
             self.landed = end
             # C: Candidate objects with their slots filled directly (hostsrc/vsmat.c)
-            self.mat.fill(self.out, self.gids_np, lo, count, lens, scores, offs, self.toks[:end], self.eng.k,
+            self.mat.fill(self.out, self.gids_np, lo, count, lens, scores, offs, self.toks[:end], stride,
                           Candidate)
 
     def finish(self, st) -> list:
         """After the run's final status (synchronised): request the rest, wait."""
         fill = int(st[N.ST_TOKFILL])
         if self.lo < self.eng.N or fill > self.tok_hi:
-            self._request(self.eng.N, fill)
+            self._request(self.eng.N, fill, compact=True)
         self.poll(block=True)
         return self.out
 

@@ -17,6 +17,7 @@
  *     scores  float64[nq*k]  fp64 scores
  *     offs    int32[nq*k]    start of each candidate's tokens in toks
  *     toks    int32[*]       the host copy of out_tok (absolute offsets)
+ *     k = 0: lens/scores/offs hold only the emitted candidates, consecutive
  *
  *   fill_packed(out, gids, count, lens, scores, toks, Candidate)
  *     the packed layout of the multi-GPU gather: each input's candidates are
@@ -101,7 +102,8 @@ static PyObject* fill(PyObject* self, PyObject* args) {
   const double* sc = (const double*)scores.buf;
   const int32_t* of = (const int32_t*)offs.buf;
   const int32_t* tk = (const int32_t*)toks.buf;
-  const Py_ssize_t ntok = toks.len / 4, nq = count.len / 4, nout = PyList_GET_SIZE(out);
+  const Py_ssize_t ntok = toks.len / 4, nq = count.len / 4, nout = PyList_GET_SIZE(out), ne = lens.len / 4;
+  Py_ssize_t run = 0;
   for (Py_ssize_t q = 0; q < nq; ++q) {
     const long long gi = has_gids ? ((const long long*)gids.buf)[lo + q] : (long long)(lo + q);
     if (gi < 0 || gi >= nout) {
@@ -109,14 +111,14 @@ static PyObject* fill(PyObject* self, PyObject* args) {
       goto done;
     }
     const int c = cnt[q];
-    if (c < 0 || c > k) {
+    if (c < 0 || (k > 0 && c > k) || (k == 0 && run + c > ne) || (k > 0 && (q + 1) * k > ne)) {
       PyErr_SetString(PyExc_ValueError, "bad candidate count");
       goto done;
     }
     PyObject* per = PyList_New(c);
     if (!per) goto done;
     for (int e = 0; e < c; ++e) {
-      const Py_ssize_t j = q * k + e;
+      const Py_ssize_t j = k > 0 ? q * k + e : run++;  /* k == 0: compacted, consecutive */
       const Py_ssize_t b = of[j], n = ln[j];
       if (n < 0 || b < 0 || b + n > ntok) {
         Py_DECREF(per);

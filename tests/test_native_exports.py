@@ -151,3 +151,22 @@ def test_host_materialisation_extension_builds_candidates():
     with pytest.raises(ValueError):
         mat.fill(out, None, 0, count, lens, scores, np.array([2, 99, 0, 5, 0, 0], dtype=np.int32), toks, k,
                  Candidate)
+
+
+def test_host_materialisation_compacted_layout():
+    """fill with k = 0: only the emitted candidates' metadata, consecutive."""
+    import numpy as np
+
+    from paper_2010_02164_b200 import _native
+    from paper_2010_02164_b200.core import Candidate
+
+    mat = _native.load_vsmat()
+    toks = np.array([9, 0, 5, 2, 0, 7, 1, 0, 4], dtype=np.int32)
+    out = [None] * 2
+    mat.fill(out, None, 0, np.array([2, 1], dtype=np.int32), np.array([3, 2, 3], dtype=np.int32),
+             np.array([-1.0, -2.0, -3.0]), np.array([1, 7, 4], dtype=np.int32), toks, 0, Candidate)
+    assert out[0] == [Candidate((0, 5, 2), -1.0, True, 0), Candidate((0, 4), -2.0, True, 0)]
+    assert out[1] == [Candidate((0, 7, 1), -3.0, True, 1)]
+    with pytest.raises(ValueError):
+        mat.fill(out, None, 0, np.array([3, 1], dtype=np.int32), np.array([3, 2, 3], dtype=np.int32),
+                 np.array([-1.0, -2.0, -3.0]), np.array([1, 7, 4], dtype=np.int32), toks, 0, Candidate)
