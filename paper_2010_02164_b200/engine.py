@@ -337,12 +337,19 @@ class SearchEngine:
         N.check(self.lib.vs_beam_step(C.byref(self.cfg), C.byref(self.state), self.m_rows,
                                       self.stream_ptr), "vs_beam_step")
 
+    _FUSED = os.environ.get("VS_FUSED_SCHED", "1") != "0"
+
     def beam_step_schedule(self, *, admit: int, select: int, mirror: int | None = None) -> None:
         """K2 with K3 fused into its last CTA: this step's prune/finalise plus
-        the next step's removal, refill, selection and row list."""
-        N.check(self.lib.vs_beam_step_schedule(C.byref(self.cfg), C.byref(self.state), self.m_rows, self.N,
-                                               admit, select, mirror, self.stream_ptr),
-                "vs_beam_step_schedule")
+        the next step's removal, refill, selection and row list (VS_FUSED_SCHED=0:
+        the same work as two launches, K2 then the standalone K3)."""
+        if self._FUSED:
+            N.check(self.lib.vs_beam_step_schedule(C.byref(self.cfg), C.byref(self.state), self.m_rows, self.N,
+                                                   admit, select, mirror, self.stream_ptr),
+                    "vs_beam_step_schedule")
+        else:
+            self.beam_step()
+            self.schedule(first=False, remove=True, admit=admit, select=select, mirror=mirror)
 
     def status_ptr(self, idx: int) -> int:
         return self.t["status"].data_ptr() + 4 * idx
