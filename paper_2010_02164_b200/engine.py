@@ -33,6 +33,7 @@ import torch
 from . import _native as N
 from .core import Candidate, DecodeConfig, FinalizationPolicy, Vocabulary
 from .errors import ConfigError, InvariantViolation
+from .harness import check_corpus, flatten
 from .metrics import CostParams, MetricsReport
 
 
@@ -223,11 +224,9 @@ class SearchEngine:
         Pass ``src_tok``/``src_off`` (pinned host or device int32) to skip the
         Python flattening."""
         if src_off is None:
-            lens = np.fromiter((len(x) for x in corpus), dtype=np.int64, count=len(corpus))
-            src_off = np.zeros(len(corpus) + 1, dtype=np.int32)
-            np.cumsum(lens, out=src_off[1:])
-            src_tok = np.fromiter(itertools.chain.from_iterable(corpus), dtype=np.int32,
-                                  count=int(src_off[-1]))  # C-level flattening
+            src_tok, src_off = flatten(corpus, dtype=np.int64)
+            check_corpus(src_tok, src_off, self.vocab.size)  # bb/model.py:90-102, before any launch
+            src_tok = src_tok.astype(np.int32)
         if isinstance(src_off, np.ndarray):
             src_off, src_tok = torch.from_numpy(src_off), torch.from_numpy(src_tok)
         n_in = int(src_off.shape[0]) - 1

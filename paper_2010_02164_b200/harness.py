@@ -11,6 +11,7 @@ stays sorted and length-balanced and keeps its global input ids.
 
 from __future__ import annotations
 
+import itertools
 import math
 import random
 from dataclasses import dataclass
@@ -66,12 +67,29 @@ def shard(n_items: int, world: int, rank: int) -> np.ndarray:
     return idx[owner == rank]
 
 
-def flatten(corpus) -> tuple[np.ndarray, np.ndarray]:
-    """(src_tok int32 [total], src_off int32 [N+1]) for SearchEngine.load_corpus."""
+def check_corpus(tok: np.ndarray, off: np.ndarray, vocab_size: int) -> None:
+    """The reference's input checks (bb/model.py:90-102 _check_input_tokens,
+    run at encode time there) over a flattened corpus at once: every input
+    nonempty, every token inside the vocabulary; raises DataError with the
+    reference's messages."""
+    lens = np.diff(off)
+    if (lens <= 0).any():
+        raise DataError("inputs must be nonempty")
+    bad = np.flatnonzero((tok < 0) | (tok >= vocab_size))
+    if bad.size:
+        j = int(bad[0])
+        i = int(np.searchsorted(off, j, side="right")) - 1
+        raise DataError(f"token {int(tok[j])} at position {j - int(off[i])} is outside the vocabulary "
+                        f"(size {vocab_size})")
+
+
+def flatten(corpus, dtype=np.int32) -> tuple[np.ndarray, np.ndarray]:
+    """(src_tok [total], src_off int32 [N+1]) for SearchEngine.load_corpus
+    (tokens as `dtype`: int64 to range-check them before narrowing)."""
     lens = np.fromiter((len(x) for x in corpus), dtype=np.int64, count=len(corpus))
     off = np.zeros(len(corpus) + 1, dtype=np.int32)
     np.cumsum(lens, out=off[1:])
-    tok = np.fromiter((t for x in corpus for t in x), dtype=np.int32, count=int(off[-1]))
+    tok = np.fromiter(itertools.chain.from_iterable(corpus), dtype=dtype, count=int(off[-1]))
     return tok, off
 
 

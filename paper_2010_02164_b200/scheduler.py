@@ -11,13 +11,15 @@ be a BatchedScorer (device) or any reference-protocol Scorer
 from __future__ import annotations
 
 import math
+
+import numpy as np
 import torch
 
 from . import _native as N
 from .core import Candidate, DecodeConfig, Vocabulary
 from .engine import SearchEngine, drive_concurrent
 from .errors import ConfigError
-from .harness import shard
+from .harness import check_corpus, flatten, shard
 from .metrics import CostParams, MetricsReport, merge_reports
 from .scorers import HostScorerAdapter
 
@@ -66,16 +68,25 @@ def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
     concurrently on separate CUDA streams of one device.  Every input's output
     is independent of batch composition (bb SPEC.md:379), so the candidates
     equal a single-batch run's; the MetricsReport sums the batches' counters."""
+    # flattened once; the reference's input checks over the whole corpus
+    # before any batch launches
+    tok, off = flatten(corpus, dtype=np.int64)
+    check_corpus(tok, off, _vocab(scorer).size)
+    tok = tok.astype(np.int32)
+    lens = np.diff(off)
     shards = [shard(len(corpus), streams, q) for q in range(streams)]
     out = [[] for _ in range(len(corpus))]
     engines, jobs = [], []
     for q in range(streams):
         eng, stream = _engine(config, _vocab(scorer), q)
         sc = scorer if q == 0 else _fork_for(eng, scorer)
-        sub = [corpus[int(i)] for i in shards[q]]
+        ids = np.asarray(shards[q], dtype=np.int64)
+        sub_off = np.zeros(len(ids) + 1, dtype=np.int32)
+        np.cumsum(lens[ids], out=sub_off[1:])
+        gather = np.repeat(off[ids].astype(np.int64) - sub_off[:-1], lens[ids]) + np.arange(int(sub_off[-1]))
         # outputs stream into `out` (global ids) while the batches decode
-        gen = eng.async_steps(sub, sc, admit_mode=admit, select_mode=select, trace=trace,
-                              harvest_into=out, gids=shards[q])
+        gen = eng.async_steps(None, sc, admit_mode=admit, select_mode=select, trace=trace,
+                              src_tok=tok[gather], src_off=sub_off, harvest_into=out, gids=shards[q])
         engines.append(eng)
         jobs.append((stream, gen))
     reports = drive_concurrent(jobs)

@@ -134,3 +134,19 @@ def test_cli_rejects_out_of_scope_model_kinds(tmp_path):
     cp.write_text("3 4 5\n")
     assert cli.main(["--engine", "varstream", "--k", "2", "--n", "2", "--model", str(mp),
                      "--corpus", str(cp)]) == 2
+
+
+def test_corpus_checks_match_reference_messages():
+    """harness.check_corpus (run by the engine before a decode) raises the
+    reference's DataErrors (bb/model.py:90-102)."""
+    import numpy as np
+
+    from paper_2010_02164_b200.harness import check_corpus
+
+    check_corpus(np.array([1, 2, 3]), np.array([0, 2, 3]), 10)
+    with pytest.raises(DataError, match="inputs must be nonempty"):
+        check_corpus(np.array([1, 2]), np.array([0, 2, 2]), 10)
+    with pytest.raises(DataError, match=r"token 12 at position 1 is outside the vocabulary \(size 10\)"):
+        check_corpus(np.array([1, 2, 3, 12]), np.array([0, 2, 4]), 10)
+    with pytest.raises(DataError, match="token -1 at position 0"):
+        check_corpus(np.array([-1]), np.array([0, 1]), 10)

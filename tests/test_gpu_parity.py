@@ -999,3 +999,21 @@ def test_streamed_output_harvest_matches_synchronous_results(chunk):
     assert [[(c.tokens, c.score, c.input_id) for c in per] for per in out] == \
         [[(c.tokens, c.score, c.input_id) for c in per] for per in want]
     assert eng.last_d2h_bytes > 0
+
+
+@pytest.mark.gpu
+def test_device_path_rejects_bad_inputs_like_reference():
+    """Empty inputs / out-of-vocabulary tokens raise the reference's DataErrors
+    (bb/model.py:90-102) on the device path, before any kernel runs, for both
+    the single-batch and the concurrent-batch drivers."""
+    P, _, _, DeviceHashScorer, _, _ = _pkg()
+    vocab = P.Vocabulary(16, 0, 2)
+    cfg = P.DecodeConfig(k=2, n=2, epsilon=1 / 6, max_candidates=2, max_len=8)
+    sc = DeviceHashScorer(vocab, 5)
+    for streams in (1, 2):
+        with pytest.raises(P.DataError, match="inputs must be nonempty"):
+            P.run_varstream([[3, 4], [], [5]], sc, cfg, streams=streams)
+        with pytest.raises(P.DataError, match=r"token 16 at position 2 is outside the vocabulary \(size 16\)"):
+            P.run_varstream([[3, 4], [5, 6, 16], [5]], sc, cfg, streams=streams)
+    out, _ = P.run_varstream([[3, 4], [5, 6, 7], [5]], sc, cfg)  # the engine is still usable
+    assert len(out) == 3 and all(out)
