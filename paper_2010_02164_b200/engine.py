@@ -33,7 +33,7 @@ import torch
 from . import _native as N
 from .core import Candidate, DecodeConfig, FinalizationPolicy, Vocabulary
 from .errors import ConfigError, InvariantViolation
-from .harness import check_corpus, flatten
+from .harness import flatten_checked
 from .metrics import CostParams, MetricsReport
 
 
@@ -224,9 +224,7 @@ class SearchEngine:
         Pass ``src_tok``/``src_off`` (pinned host or device int32) to skip the
         Python flattening."""
         if src_off is None:
-            src_tok, src_off = flatten(corpus, dtype=np.int64)
-            check_corpus(src_tok, src_off, self.vocab.size)  # bb/model.py:90-102, before any launch
-            src_tok = src_tok.astype(np.int32)
+            src_tok, src_off = flatten_checked(corpus, self.vocab.size)  # bb/model.py:90-102, before any launch
         if isinstance(src_off, np.ndarray):
             src_off, src_tok = torch.from_numpy(src_off), torch.from_numpy(src_tok)
         n_in = int(src_off.shape[0]) - 1

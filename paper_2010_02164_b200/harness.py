@@ -93,6 +93,21 @@ def flatten(corpus, dtype=np.int32) -> tuple[np.ndarray, np.ndarray]:
     return tok, off
 
 
+def flatten_checked(corpus, vocab_size: int) -> tuple[np.ndarray, np.ndarray]:
+    """flatten + check_corpus for the device upload: (src_tok int32, src_off
+    int32), one C pass (host extension _vsmat.flatten) instead of Python
+    iteration; on any rejected input the numpy path re-checks and raises the
+    reference's DataError (bb/model.py:90-102)."""
+    from ._native import load_vsmat
+
+    res = load_vsmat().flatten(corpus, int(vocab_size))
+    if res is not None and res[2]:
+        return np.frombuffer(res[0], dtype=np.int32), np.frombuffer(res[1], dtype=np.int32)
+    tok, off = flatten(corpus, dtype=np.int64)
+    check_corpus(tok, off, vocab_size)
+    return tok.astype(np.int32), off
+
+
 # ---------------------------------------------------------------- file formats
 # Drop-in for the reference's experiment I/O (bb/harness.py:47-69 corpus text,
 # :170-206 results JSON, :209-219 trace CSV, :280-331 run_experiment).

@@ -22,6 +22,12 @@
  *   fill_packed(out, gids, count, lens, scores, toks, Candidate)
  *     the packed layout of the multi-GPU gather: each input's candidates are
  *     consecutive in lens/scores and their tokens consecutive in toks
+ *
+ *   flatten(corpus, V) -> (tok bytearray int32[total], off bytearray int32[N+1], ok)
+ *     the corpus (a sequence of token sequences) flattened in one C pass for
+ *     the device upload; ok = 0 when an input is empty or a token is outside
+ *     [0, V) (the caller re-checks to raise the reference's DataError); None
+ *     when an item is not a sequence of ints (the caller's generic path)
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
@@ -229,7 +235,94 @@ done:
   return ret;
 }
 
+static PyObject* flatten(PyObject* self, PyObject* args) {
+  PyObject* corpus;
+  long long V;
+  if (!PyArg_ParseTuple(args, "OL", &corpus, &V)) return NULL;
+  PyObject* seq = PySequence_Fast(corpus, "corpus must be a sequence");
+  if (!seq) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  PyObject** items = PySequence_Fast_ITEMS(seq);
+  PyObject *off = NULL, *tok = NULL, *ret = NULL;
+  off = PyByteArray_FromStringAndSize(NULL, (n + 1) * (Py_ssize_t)sizeof(int32_t));
+  if (!off) goto done;
+  int32_t* po = (int32_t*)PyByteArray_AS_STRING(off);
+  long long total = 0;
+  po[0] = 0;
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* it = items[i];
+    Py_ssize_t L;
+    if (PyTuple_CheckExact(it)) L = PyTuple_GET_SIZE(it);
+    else if (PyList_CheckExact(it)) L = PyList_GET_SIZE(it);
+    else {
+      L = PySequence_Size(it);
+      if (L < 0) {
+        PyErr_Clear();
+        Py_INCREF(Py_None);
+        ret = Py_None;
+        goto done;
+      }
+    }
+    total += L;
+    if (total > 0x7fffffffLL) {
+      PyErr_SetString(PyExc_OverflowError, "corpus has more than 2^31-1 tokens");
+      goto done;
+    }
+    po[i + 1] = (int32_t)total;
+  }
+  tok = PyByteArray_FromStringAndSize(NULL, (Py_ssize_t)total * (Py_ssize_t)sizeof(int32_t));
+  if (!tok) goto done;
+  int32_t* pt = (int32_t*)PyByteArray_AS_STRING(tok);
+  int ok = 1;
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* it = items[i];
+    const Py_ssize_t L = po[i + 1] - po[i];
+    if (L == 0) ok = 0;
+    PyObject* f = PySequence_Fast(it, "input must be a sequence");
+    if (!f) {
+      PyErr_Clear();
+      Py_INCREF(Py_None);
+      ret = Py_None;
+      goto done;
+    }
+    if (PySequence_Fast_GET_SIZE(f) != L) {  /* changed under us */
+      Py_DECREF(f);
+      Py_INCREF(Py_None);
+      ret = Py_None;
+      goto done;
+    }
+    PyObject** e = PySequence_Fast_ITEMS(f);
+    int32_t* dst = pt + po[i];
+    for (Py_ssize_t j = 0; j < L; ++j) {
+      long long t;
+#if PY_VERSION_HEX >= 0x030C0000
+      if (PyLong_CheckExact(e[j]) && PyUnstable_Long_IsCompact((PyLongObject*)e[j]))
+        t = (long long)PyUnstable_Long_CompactValue((PyLongObject*)e[j]);
+      else
+#endif
+        t = PyLong_AsLongLong(e[j]);
+      if (t == -1 && PyErr_Occurred()) {
+        PyErr_Clear();
+        Py_DECREF(f);
+        Py_INCREF(Py_None);
+        ret = Py_None;
+        goto done;
+      }
+      if (t < 0 || t >= V) ok = 0;
+      dst[j] = (int32_t)t;
+    }
+    Py_DECREF(f);
+  }
+  ret = Py_BuildValue("(OOi)", tok, off, ok);
+done:
+  Py_XDECREF(tok);
+  Py_XDECREF(off);
+  Py_DECREF(seq);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
+    {"flatten", flatten, METH_VARARGS, "Flatten a corpus to int32 tokens + offsets, range-checked."},
     {"fill", fill, METH_VARARGS, "Build Candidate lists for a chunk of decoded inputs."},
     {"reserve", reserve, METH_VARARGS, "Cache the int objects of token ids [0, V)."},
     {"fill_packed", fill_packed, METH_VARARGS, "Build Candidate lists from a packed (gathered) shard."},

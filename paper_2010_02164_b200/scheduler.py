@@ -19,7 +19,7 @@ from . import _native as N
 from .core import Candidate, DecodeConfig, Vocabulary
 from .engine import SearchEngine, drive_concurrent
 from .errors import ConfigError
-from .harness import check_corpus, flatten, shard
+from .harness import flatten_checked, shard
 from .metrics import CostParams, MetricsReport, merge_reports
 from .scorers import HostScorerAdapter
 
@@ -70,9 +70,7 @@ def _run_concurrent(corpus, scorer, config, admit, select, trace, streams):
     equal a single-batch run's; the MetricsReport sums the batches' counters."""
     # flattened once; the reference's input checks over the whole corpus
     # before any batch launches
-    tok, off = flatten(corpus, dtype=np.int64)
-    check_corpus(tok, off, _vocab(scorer).size)
-    tok = tok.astype(np.int32)
+    tok, off = flatten_checked(corpus, _vocab(scorer).size)
     lens = np.diff(off)
     shards = [shard(len(corpus), streams, q) for q in range(streams)]
     out = [[] for _ in range(len(corpus))]

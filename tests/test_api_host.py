@@ -93,3 +93,29 @@ def test_merge_reports_sums_counters_and_renumbers_trace():
     assert m.simulated_cost == a.simulated_cost + b.simulated_cost
     assert [r.timestep for r in m.per_step_trace] == [1, 2, 3, 4, 5]
     assert [(r.expansions, r.effective_len) for r in m.per_step_trace] == [(4, 1), (6, 2), (3, 1), (5, 2), (2, 3)]
+
+
+def test_flatten_checked_matches_numpy_path_and_reference_errors():
+    """The C corpus flattening for the device upload (_vsmat.flatten) equals
+    the numpy path and rejects inputs with the reference's DataErrors
+    (bb/model.py:90-102): empty input, token outside [0, V), non-int items."""
+    import numpy as np
+
+    from paper_2010_02164_b200.errors import DataError
+    from paper_2010_02164_b200.harness import flatten, flatten_checked
+
+    rng = random.Random(3)
+    corpus = [tuple(rng.randrange(50) for _ in range(rng.randrange(1, 30))) for _ in range(300)]
+    corpus += [list(c) for c in corpus[:20]] + [range(3, 9)]
+    tok, off = flatten_checked(corpus, 50)
+    wt, wo = flatten(corpus)
+    assert tok.dtype == np.int32 and off.dtype == np.int32
+    assert np.array_equal(tok, wt) and np.array_equal(off, wo)
+    with pytest.raises(DataError, match="nonempty"):
+        flatten_checked([(1, 2), ()], 50)
+    with pytest.raises(DataError, match="token 50 at position 1 is outside"):
+        flatten_checked([(1, 2), (3, 50)], 50)
+    with pytest.raises(DataError, match="token -1 at position 0"):
+        flatten_checked([(-1,)], 50)
+    t2, o2 = flatten_checked([[np.int64(5), 6], (7,)], 50)
+    assert t2.tolist() == [5, 6, 7] and o2.tolist() == [0, 2, 3]

@@ -373,6 +373,39 @@ def test_device_hash_decode_matches_oracle(case):
     assert fast_rep.per_step_trace == rep.per_step_trace
 
 
+HASH_LOGIT_CASES = [
+    # V, k, n, dtype, scale, power, eos_bias, N: enough rows per step that a
+    # CTA walks several rows (grid = column chunks x row groups); tiny V (one
+    # chunk, ragged tail group), the WMT vocabulary, every power mode
+    (42024, 16, 64, "bf16", 0.5, 0, 7.5, 80),
+    (42024, 8, 32, "f32", 0.5, 0, 7.5, 40),
+    (1003, 12, 48, "bf16", 8.0, 1, 6.0, 120),
+    (5000, 6, 40, "f32", 6.0, 2, 5.0, 80),
+    (3001, 6, 40, "bf16", 10.0, 4, 9.0, 80),
+]
+
+
+@pytest.mark.parametrize("case", HASH_LOGIT_CASES, ids=lambda c: f"V{c[0]}_{c[3]}_p{c[5]}")
+def test_device_hash_logits_bit_exact(case):
+    """Every logit of every scored row (not only the ones that reach a
+    decision) equals the CPU mirror oracle/scorers.py:HashLogitsCPU bit for
+    bit: admitted rows (inline encode) and extended rows, the EOS column, the
+    ragged vocabulary tail."""
+    V, k, n, dt, scale, power, eb, Nin = case
+    P, N, SearchEngine, DeviceHashScorer, _, LseRecorder = _pkg()
+    vocab = P.Vocabulary(V, 0, 2)
+    cfg = P.DecodeConfig(k=k, n=n, epsilon=1 / 6, delta=3.0, max_candidates=4, max_len=12)
+    corpus, _ = O.bucket_by_length(O.generate_synthetic_corpus(5, Nin, V, mean_len=6.0, clip=20))
+    rec = LseRecorder(DeviceHashScorer(vocab, 11, scale=scale, power=power, eos_bias=eb, dtype=dt),
+                      record_logits=True)
+    P.run_varstream(corpus, rec, cfg)
+    cpu = HashLogitsCPU(V, 0, 2, 11, scale=scale, power=power, eos_bias=eb, dtype=dt)
+    assert len(rec.logit_table) > 4 * n
+    for (iid, toks), got in rec.logit_table.items():
+        want = cpu.logits(cpu.encode(corpus[iid], iid), toks)
+        assert np.array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32)), (iid, toks)
+
+
 # The bench's own workloads (bench.py WORKLOADS) at their exact engine shapes:
 # name, V, k, n, M, delta, max_len, N (a prefix of the bench's corpus
 # generator: geometric, seed 99), mean_len, clip, scorer seed, scale, eos_bias
