@@ -425,7 +425,7 @@ def lstm_reference(w, n_inputs: int = 64, procs: int | None = None):
 
     from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
     from paper_2010_02164_b200.decoder import LSTMScorer
-    from oracle.agreement import compare
+    from oracle.agreement import compare_detail, summarize
 
     corpus = _corpus(w)
     stride = max(1, len(corpus) // n_inputs)
@@ -440,17 +440,13 @@ def lstm_reference(w, n_inputs: int = 64, procs: int | None = None):
     cfg = DecodeConfig(k=w["k"], n=w["n"], epsilon=w["eps"], delta=w["delta"], max_candidates=w["M"],
                        max_len=w["max_len"])
     gpu, _ = run_varstream(sample, LSTMScorer(vocab, **LSTM_KW), cfg)
-    same = top1 = 0
-    for q in range(len(sample)):
-        s_, t_ = compare([(c.tokens, c.score) for c in gpu[q]], cpu[q])
-        same += s_
-        top1 += t_
+    agree = summarize([compare_detail([(c.tokens, c.score) for c in gpu[q]], cpu[q]) for q in range(len(sample))])
     n = len(sample)
     return ({"value": round(n / busy, 3), "unit": "seq/s", "cores": procs, "kind": "port",
              "sample": f"{n} of {len(corpus)} inputs (every {stride}th of the length-sorted corpus), {procs} "
                        f"processes x 1 thread, the reference search + CPU LSTM (stateless prefix recompute, "
                        f"fp64 rows), slowest {busy:.1f}s"},
-            {"inputs": n, "identical_fraction": round(same / n, 4), "top1_fraction": round(top1 / n, 4),
+            {"inputs": n, **agree,
              "reference": "oracle beam_decode + LSTMDecoderCPU (same random-init weights, bf16-rounded operands, "
                           "fp32 compute, fp64 log-softmax rows)"})
 
@@ -550,7 +546,7 @@ def decoder_agreement(w, n_inputs: int = 64, procs: int | None = None, precision
 
     from paper_2010_02164_b200 import DecodeConfig, Vocabulary, run_varstream
     from paper_2010_02164_b200.decoder import GraphedTransformerScorer, TransformerScorer
-    from oracle.agreement import compare
+    from oracle.agreement import compare_detail, summarize
 
     corpus = _corpus(w)
     stride = max(1, len(corpus) // n_inputs)
@@ -583,18 +579,16 @@ def decoder_agreement(w, n_inputs: int = 64, procs: int | None = None, precision
     with mp.get_context("spawn").Pool(procs) as pool:
         res = [r for part in pool.map(_dec_agree_worker, [(w, c, weights) for c in chunks]) for r in part]
     wall = time.perf_counter() - t0
-    same = top1 = 0
-    div = []
+    details, div = [], []
     for q, want, margin in sorted(res):
-        got = [(c.tokens, c.score) for c in gpu[q]]
-        s_, t_ = compare(got, want)
-        same += s_
-        top1 += t_
-        if not s_:
-            div.append({"input": ids[q], "top1_same": bool(t_), "reference_margin": float(f"{margin:.3g}")})
+        d_ = compare_detail([(c.tokens, c.score) for c in gpu[q]], want)
+        details.append(d_)
+        if not d_["sequences"]:
+            div.append({"input": ids[q], "top1_same": d_["top1"], "same_set": d_["set"],
+                        "reference_margin": float(f"{margin:.3g}")})
     n = len(sample)
-    return {"inputs": n, "precision": precision, "identical_fraction": round(same / n, 4),
-            "top1_fraction": round(top1 / n, 4), "divergent": len(div), "divergences": div,
+    return {"inputs": n, "precision": precision, **summarize(details),
+            "divergent_sequences": len(div), "divergences": div,
             "device_model": "GraphedTransformerScorer, bf16 (the bench leg's model)" if precision == "bf16" else
                             "TransformerScorer fp32 (TF32 off), same weights",
             "reference": "oracle beam_decode (bb/search.py:233-242) + TorchDecoderCPU (same random-init weights"

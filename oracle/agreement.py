@@ -40,6 +40,34 @@ def compare(got, want, rel: float = 1e-5):
     return same, top1
 
 
+def compare_detail(got, want, rel: float = 1e-5) -> dict:
+    """Per-input agreement classes (got/want: per-input lists of (tokens, score)):
+    ``sequences`` — the same decoded token sequences in the same order (north_star:
+    "decoded sequences match"); ``set`` — the same sequences, order aside (a swap of
+    two near-equal scores); ``scores`` — sequences identical and every score within
+    ``rel`` relative; ``top1``; ``max_rel`` — the largest relative score difference
+    over a sequence-identical input (None otherwise)."""
+    ta = [tuple(a[0]) for a in got]
+    tb = [tuple(b[0]) for b in want]
+    seq = ta == tb
+    worst = None
+    if seq:
+        worst = max((abs(a[1] - b[1]) / max(1.0, abs(b[1])) for a, b in zip(got, want)), default=0.0)
+    return {"sequences": seq, "set": sorted(ta) == sorted(tb), "scores": seq and worst <= rel,
+            "top1": bool(ta) and bool(tb) and ta[0] == tb[0], "max_rel": worst}
+
+
+def summarize(details: list) -> dict:
+    """Fractions over compare_detail results (the agreement report's keys)."""
+    n = max(1, len(details))
+    rels = [d["max_rel"] for d in details if d["max_rel"] is not None]
+    return {"sequences_identical_fraction": round(sum(d["sequences"] for d in details) / n, 4),
+            "sequence_set_identical_fraction": round(sum(d["set"] for d in details) / n, 4),
+            "identical_fraction": round(sum(d["scores"] for d in details) / n, 4),
+            "top1_fraction": round(sum(d["top1"] for d in details) / n, 4),
+            "max_rel_score_diff_of_identical_sequences": float(f"{max(rels):.3g}") if rels else None}
+
+
 def decision_margin(encoding, scorer, cfg: O.OConfig) -> float:
     """Smallest decision margin of the reference's deferred-policy search for
     one input (see module docstring)."""

@@ -160,7 +160,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
   __syncthreads();
   const int P = nfz + nact * Meff;
 
-  VS_PROF(blockIdx.x == 0, 1);
+  VS_PROF(true, 1);
   // ---- pool (bb/search.py:64-72): no-ops, then per-parent top-M ----------------
   for (int e = tid; e < P; e += NT2) {
     if (e < nfz) {
@@ -203,7 +203,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
   __syncthreads();
   const Pool pool{ps, pp, pt};
   const int NL = nfz + nact;  // == w lists
-  VS_PROF(blockIdx.x == 0, 2);
+  VS_PROF(true, 2);
   // ---- rank-0 entry = best list head (warp 0) -> δ cutoff ------------------------
   if (wid == 0) {
     int best = -1;
@@ -271,7 +271,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     nkept = s_kept;  // ranks 0..nkept-1 are filled (contiguous prefix)
   }
 
-  VS_PROF(blockIdx.x == 0, 3);
+  VS_PROF(true, 3);
   // ---- materialise children (thread j = child j) --------------------------------
   const int j = tid;
   const bool child = j < nkept;
@@ -327,7 +327,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     ctok[j] = tk;
     prow[j] = cr[pi];  // a no-op's own row, else the parent's (prefix [0, L))
   }
-  VS_PROF(blockIdx.x == 0, 4);
+  VS_PROF(true, 4);
   // ---- deferred emission + length-cap drain ------------------------------------
   const int emitted0 = st.slot_emitted[s];
   int first, ne, width;
@@ -366,7 +366,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     if (j < ne) eoff[j] = s_ebase + epre;
     __syncthreads();
   }
-  VS_PROF(blockIdx.x == 0, 5);
+  VS_PROF(true, 5);
   // ---- token histories + emission, one flattened phase ---------------------------
   // Every read is of a claimed row's prefix [0, L) (a parent's, or a no-op's own
   // row), every write goes to a free row or to position L, so the prefix copies
@@ -412,7 +412,7 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
     }
   }
 
-  VS_PROF(blockIdx.x == 0, 6);
+  VS_PROF(true, 6);
   // ---- next beam SoA, KV copy plan, slot state ---------------------------------
   const bool stays = child && j >= first && j < first + width;
   if (stays) {
@@ -745,14 +745,15 @@ template <bool IMM>
 __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows, int sched, int N,
                                                         int admit_mode, int select_mode, int32_t* mirror) {
   VS_PDL_ENTRY();
-  VS_PROF_T0(blockIdx.x == 0);
+  VS_PROF_T0(true);
   extern __shared__ __align__(16) unsigned char smem[];
   if ((int)blockIdx.x < st.status[VS_ST_NSEL]) {
     if (IMM) beam_immediate(cfg, st, M_rows, smem);
     else beam_deferred(cfg, st, M_rows, smem);
   }
   __syncthreads();
-  VS_PROF(blockIdx.x == 0, 7);
+  VS_PROF(true, 7);
+  VS_PROF_MAX_FOLD();
   // Grid completion: every other CTA signals its arrival; CTA 0 (always the
   // same CTA, so the scheduler's code stays warm in one SM's instruction
   // cache from step to step) waits for them, publishes the step's copy count
@@ -779,6 +780,7 @@ __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state 
   }
   __syncthreads();
   VS_PROF(true, 8);
+  VS_PROF_MAX_COLLECT();
   if (sched)
     schedule_block<NT2>(cfg, st, N, 0, 1, admit_mode, select_mode, mirror, reinterpret_cast<int*>(smem));
   VS_PROF(true, 15);

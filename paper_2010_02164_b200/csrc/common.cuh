@@ -176,10 +176,27 @@ static __shared__ long long s_prof[32];
       if (s_prof[_q]) atomicAdd(&g_prof_acc[_q], (unsigned long long)(s_prof[_q] - s_prof[0])); \
     atomicAdd(&g_prof_acc[31], 1ull);                                              \
   }
+// Slowest-CTA view: every probing CTA folds its own stamps 1..7 (cycles since
+// its start) into g_prof_max with atomicMax before it counts in; the CTA that
+// runs the scheduler moves the per-launch maxima into g_prof_acc[16 + i].
+static __device__ unsigned long long g_prof_max[8];
+#define VS_PROF_MAX_FOLD()                                                          \
+  if (threadIdx.x == 0) {                                                           \
+    for (int _q = 1; _q < 8; ++_q)                                                  \
+      if (s_prof[_q]) atomicMax(&g_prof_max[_q], (unsigned long long)(s_prof[_q] - s_prof[0])); \
+  }
+#define VS_PROF_MAX_COLLECT()                                                       \
+  if (threadIdx.x == 0) {                                                           \
+    for (int _q = 1; _q < 8; ++_q) {                                                \
+      atomicAdd(&g_prof_acc[16 + _q], atomicExch(&g_prof_max[_q], 0ull));          \
+    }                                                                               \
+  }
 #else
 #define VS_PROF_T0(cond) (void)0
 #define VS_PROF(cond, i) (void)0
 #define VS_PROF_FLUSH(cond) (void)0
+#define VS_PROF_MAX_FOLD() (void)0
+#define VS_PROF_MAX_COLLECT() (void)0
 #endif
 
 #define VS_CUDA_RET()                                              \

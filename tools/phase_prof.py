@@ -64,3 +64,6 @@ print(f"{n} fused launches ({rep.timesteps} steps); CTA 0 (beam 0, then the sche
       "since it started:")
 for i, name in NAMES.items():
     print(f"  {i:2d} {name:28s} {acc[i] / n:9.0f}")
+print("slowest beam CTA per launch (max over CTAs of cycles since that CTA started), mean over launches:")
+for i in range(1, 8):
+    print(f"  {i:2d} {NAMES[i]:28s} {acc[16 + i] / n:9.0f}")
