@@ -101,11 +101,28 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int k = cfg.k;
-  const int s = st.sel[b];
-  const int L = st.slot_lt[s];
-  const int w = st.slot_width[s];
-  const int row0 = st.sel_off[b];
+  // The beam's slot metadata and candidate state were written by launches that
+  // completed before the top-M kernel now finishing (the one this launch
+  // depends on) passed its own PDL wait, so they are loaded (from L2) under
+  // that kernel's tail, before this CTA's wait; only the top-M outputs
+  // (top_tok / top_logp / top_logp64) need the wait.
+  const int s = __ldcg(&st.sel[b]);
+  const int L = __ldcg(&st.slot_lt[s]);
+  const int w = __ldcg(&st.slot_width[s]);
+  const int row0 = __ldcg(&st.sel_off[b]);
   const int base = s * k;
+  double p_sc = 0.0;
+  unsigned long long p_h = 0;
+  int p_l = 0, p_r = 0;
+  bool isfin = false;
+  if (tid < w) {
+    p_sc = __ldcg(&st.c_score[base + tid]);
+    p_h = __ldcg(reinterpret_cast<const unsigned long long*>(&st.c_hash[base + tid]));
+    p_l = __ldcg(&st.c_len[base + tid]);
+    p_r = __ldcg(&st.c_row[base + tid]);
+    isfin = __ldcg(reinterpret_cast<const unsigned char*>(&st.c_fin[base + tid])) != 0;
+  }
+  VS_PDL_ENTRY();
   const int Meff = cfg.max_candidates < cfg.vocab_size ? cfg.max_candidates : cfg.vocab_size;
   const int Pmax = k + k * Meff;
 
@@ -135,13 +152,11 @@ __device__ __forceinline__ void beam_deferred(const vs_config& cfg, const vs_sta
   __shared__ double s_cut;
 
   // ---- candidates -> smem; stable finalized / active split ---------------------
-  bool isfin = false;
   if (tid < w) {
-    cs[tid] = st.c_score[base + tid];
-    ch[tid] = st.c_hash[base + tid];
-    cl[tid] = st.c_len[base + tid];
-    cr[tid] = st.c_row[base + tid];
-    isfin = st.c_fin[base + tid] != 0;
+    cs[tid] = p_sc;
+    ch[tid] = p_h;
+    cl[tid] = p_l;
+    cr[tid] = p_r;
   }
   if (tid < k) {
     firstc[tid] = 0x7fffffff;
@@ -744,10 +759,14 @@ __device__ __forceinline__ void beam_immediate(const vs_config& cfg, const vs_st
 template <bool IMM>
 __global__ void __launch_bounds__(NT2) beam_step_kernel(vs_config cfg, vs_state st, int M_rows, int sched, int N,
                                                         int admit_mode, int select_mode, int32_t* mirror) {
-  VS_PDL_ENTRY();
+  // deferred policy: the PDL wait is inside beam_deferred, after the loads of
+  // state the preceding (top-M) kernel does not write; the selected-beam count
+  // comes from the previous step's scheduler
+  const bool sel = (int)blockIdx.x < __ldcg(&st.status[VS_ST_NSEL]);
+  if (IMM || !sel) VS_PDL_ENTRY();
   VS_PROF_T0(true);
   extern __shared__ __align__(16) unsigned char smem[];
-  if ((int)blockIdx.x < st.status[VS_ST_NSEL]) {
+  if (sel) {
     if (IMM) beam_immediate(cfg, st, M_rows, smem);
     else beam_deferred(cfg, st, M_rows, smem);
   }
